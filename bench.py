@@ -1,0 +1,316 @@
+#!/usr/bin/env python3
+"""bench.py — throughput of the B200 arc/latitude intersection path (arXiv 2510.09892).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--mode eft|eft_literal|naive]
+                    [--config 2|3|5] [--impl ours|reference]
+
+One step = one launch of the whole hot path (load, accurate normal, s^2, s,
+numerators, division, containment/count, store) over one batch of synthetic arcs resident in
+HBM.  Default workload: BASELINE.json configs[1] (C2: 2^24 short arcs) per GPU; with N GPUs
+each rank owns its own 2^24-arc slice of the global index space (weak scaling, no data-path
+collective; NCCL only reduces the counts and the timing afterwards).
+
+Prints ONE JSON line on rank 0 (driver contract): metric/value/unit, roofline of the dominant
+kernel, cpu_baseline (oracle (a) on the host cores), e2e through the host-buffer C-ABI call,
+SM clocks sampled (NVML) during the timed region, and the number of our kernel launches.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "EFT arc-latitude intersections/s (FP64) at 1/2/4/8 B200; % roofline; max ulp err"
+UNIT = "intersections/s"
+BYTES_PER_ARC = 56 + 48 + 1          # a, b, z0 in; two xyz slots + uint8 count out (§8(b))
+# Algorithmic FP64 operations per query (add/sub/mul/fma/div/sqrt = 1 each) of the op sequence
+# in csrc/sgi_query.cuh; derivation in DESIGN.md §5.
+FP64_OPS = {"eft": 362, "eft_literal": 347, "naive": 42}
+SEEDS = {2: 2, 3: 3, 5: 5}
+CONFIG_DESC = {
+    2: "C2 short arcs (midpoint uniform, length log-uniform [1e-4,1e-2] rad, z0 between endpoint z)",
+    3: "C3 ill-conditioned arcs (near-tangent / near-polar / near-coincident thirds)",
+    5: "C5 mixed arcs (50% C1, 25% C2, 25% uniform endpoints with z0 uniform in [-1,1])",
+}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--mode", default="eft", choices=["eft", "eft_literal", "naive"])
+    p.add_argument("--config", type=int, default=2, choices=[2, 3, 5])
+    p.add_argument("--n", type=int, default=1 << 24, help="arcs per rank")
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--e2e-steps", type=int, default=5)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peaks = {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback (B200_PROFILING.md)"}
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        peaks.update({k: d[k] for k in ("hbm_gbs", "sm_max_mhz") if k in d})
+        peaks["source"] = "measured (MEASURED_PEAKS.json)"
+    return peaks
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons while the timed region runs."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle"}
+
+    def __init__(self, index: int, period: float = 0.002):
+        self.samples, self.reasons, self.period = [], 0, period
+        self._stop = threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover - reported, not fatal
+            self.nvml, self.err = None, str(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nvml.nvmlDeviceGetClockInfo(self.h, self.nvml.NVML_CLOCK_SM))
+                self.reasons |= self.nvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nvml:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.nvml:
+            self.t.join()
+
+    def summary(self):
+        if not self.nvml:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": self.err}
+        s = sorted(self.samples)
+        med = s[len(s) // 2] if s else None
+        names = [v for k, v in self.REASONS.items() if self.reasons & k and v != "gpu_idle"]
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(s)}
+
+
+def cpu_baseline_run(config: int, n: int, mode: str):
+    """Oracle (a) as it stands (oracle/eft_oracle.c, OpenMP over all host cores) on the whole
+    per-rank batch of the same workload; returns (arcs/s, cores, seconds)."""
+    import oracle
+    import sgi_inputs
+    cores = os.cpu_count() or 1
+    a, b, z0 = sgi_inputs.generate_host(config, n, seed=SEEDS[config])
+    m = {"eft": oracle.MODE_EFT, "eft_literal": oracle.MODE_EFT_LITERAL, "naive": oracle.MODE_NAIVE}[mode]
+    oracle.intersect(m, a[:, :4096], b[:, :4096], z0[:4096], nthreads=cores)   # warm
+    t0 = time.perf_counter()
+    oracle.intersect(m, a, b, z0, nthreads=cores)
+    dt = time.perf_counter() - t0
+    return n / dt, cores, dt
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args):
+    """--impl reference: the oracle on the host cores, each step a bounded sample (2^22 arcs)
+    of the same workload; rank 0 only."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    import sgi_inputs
+    cores = os.cpu_count() or 1
+    n = min(args.n, 1 << 22)
+    a, b, z0 = sgi_inputs.generate_host(args.config, n, seed=SEEDS[args.config])
+    m = {"eft": oracle.MODE_EFT, "eft_literal": oracle.MODE_EFT_LITERAL, "naive": oracle.MODE_NAIVE}[args.mode]
+    for _ in range(max(args.warmup, 0)):
+        oracle.intersect(m, a, b, z0, nthreads=cores)
+    steps = max(1, min(args.steps, 20))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        oracle.intersect(m, a, b, z0, nthreads=cores)
+    dt = time.perf_counter() - t0
+    value = n * steps / dt
+    sample = f"{n} arcs of config {args.config} per step (first {n} global indices), {steps} steps"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": dt / steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": CONFIG_DESC[args.config], "mode": args.mode,
+                                        "arcs_per_step": n},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2510_09892_b200 as sgi
+    import sgi_inputs
+
+    ws, rank, local = dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n, cfg, mode = args.n, args.config, args.mode
+    offset = rank * n                                   # this rank's slice of the index space
+
+    # inputs generated on this rank's device from the seed (HBM resident before timing)
+    a = torch.empty((3, n), dtype=torch.float64, device=dev)
+    b = torch.empty_like(a)
+    z0 = torch.empty(n, dtype=torch.float64, device=dev)
+    sgi_inputs.generate_device(cfg, n, a, b, z0, offset=offset, seed=SEEDS[cfg])
+    out = torch.empty((2, 3, n), dtype=torch.float64, device=dev)
+    cnt = torch.empty(n, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        sgi.intersect_arc_lat(a, b, z0, mode=mode, out_xyz=out, out_count=cnt, stream=stream)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    ms_local = e0.elapsed_time(e1)
+    t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+    hist = sgi.count_histogram(cnt)                    # outside the timed region
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(hist, op=dist.ReduceOp.SUM)
+    ms = float(t.item())
+    total_arcs = n * ws * args.steps
+    value = total_arcs / (ms * 1e-3)
+    ms_per_step = ms / args.steps
+    launch_s = ms_local * 1e-3 / args.steps             # one kernel launch per step
+
+    # roofline of the dominant (only) kernel, bound = the slower of the two roofs
+    peaks = load_peaks()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    alu_peak = sms * 64 * peaks["sm_max_mhz"] * 1e6 / 1e12     # T FP64 instr/s (64 lanes/SM)
+    hbm_bytes, ops = n * BYTES_PER_ARC, n * FP64_OPS[mode]
+    t_hbm, t_alu = hbm_bytes / (peaks["hbm_gbs"] * 1e9), ops / (alu_peak * 1e12)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            tr = json.load(f).get(f"{mode}:{cfg}:{n}")
+        traffic = tr
+    if t_alu >= t_hbm:
+        achieved = ops / launch_s / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": alu_peak,
+                "unit": "T FP64 ops/s", "frac": achieved / alu_peak, "traffic": traffic,
+                "peak_source": f"{sms} SM x 64 FP64 lanes x {peaks['sm_max_mhz']:.0f} MHz",
+                "hbm_frac": hbm_bytes / launch_s / 1e9 / peaks["hbm_gbs"]}
+    else:
+        achieved = hbm_bytes / launch_s / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                "peak_source": peaks["source"], "alu_frac": ops / launch_s / 1e12 / alu_peak}
+
+    # e2e: the host-buffer C-ABI call, pinned host inputs in, results back to the host
+    e2e = None
+    if args.e2e_steps > 0:
+        ha = a.cpu().pin_memory(); hb = b.cpu().pin_memory(); hz = z0.cpu().pin_memory()
+        hout = torch.empty((2, 3, n), dtype=torch.float64).pin_memory()
+        hcnt = torch.empty(n, dtype=torch.uint8).pin_memory()
+        work = torch.empty(sgi.host_workspace_bytes(1 << 21), dtype=torch.uint8, device=dev)
+
+        def e2e_step():
+            sgi.intersect_arc_lat_host(ha, hb, hz, mode=mode, out_xyz=hout, out_count=hcnt,
+                                       work=work, stream=stream)
+        e2e_step()
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        f1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
+        if ws > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": n * ws * args.e2e_steps / (float(te.item()) * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": n * 56 * ws, "d2h_bytes_per_step": n * 49 * ws,
+               "steps": args.e2e_steps, "path": "sgi_intersect_arc_lat_host (pinned host buffers)"}
+        del ha, hb, hz, hout, hcnt, work
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        v, cores, dt = cpu_baseline_run(cfg, n, mode)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"the full per-rank batch ({n} arcs of config {cfg}) once through oracle "
+                         f"(a) with OpenMP over {cores} threads ({dt:.2f} s)"}
+
+    if rank == 0:
+        h = hist.cpu().tolist()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": CONFIG_DESC[cfg], "mode": mode, "arcs_per_rank": n,
+                       "global_arcs_per_step": n * ws, "seed": SEEDS[cfg],
+                       "parallelism": f"arc-index shards x{ws}",
+                       "l2": f"inputs larger than L2 ({n * 56 / 1e9:.2f} GB in + "
+                             f"{n * 49 / 1e9:.2f} GB out per rank vs 126 MB L2)"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clocks.summary(),
+            "gpu_launches": args.steps,
+            "hist": {"zero": h[0], "one": h[1], "two": h[2], "degenerate": h[3], "points": h[4]},
+            "points_per_s": h[4] / (ms_per_step * 1e-3),
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,91 @@
+/* sgi.h — C ABI of libsgi.so: batched great-circle-arc / constant-latitude intersections on
+ * NVIDIA B200 (sm_100a), after Chen, Ullrich & Panetta, "Fast and Accurate Intersections on a
+ * Sphere" (arXiv 2510.09892; /root/reference/PAPER.md, cited as P:<line>).
+ *
+ * The operation (problem definition): for each query i, the great circle through
+ * the arc endpoints a_i, b_i (normal n = a_i x b_i) meets the plane z = z0_i in
+ * 0, 1 or 2 points, given by the closed form Eq.FINAL
+ *     P(+-) = ( -(z0 nx nz +- s ny) / |n_xy|^2 , -(z0 ny nz -+ s nx) / |n_xy|^2 , z0 ),
+ *     s = sqrt(|n_xy|^2 - |n|^2 z0^2).
+ * Points are kept only if they lie on the closed minor arc from a_i to b_i.
+ * Endpoints need not be unit length: the formula is invariant to |a| and |b|.
+ *
+ * Modes:
+ *   SGI_MODE_EFT          AccuX (Alg.8) with error-free transformations, both roots,
+ *                         each AccuDOP normal pair renormalised (reading R6).
+ *                         Error bound 3 sqrt(1 - z0^2) u, u = 2^-53 (Eq.BOUND).
+ *   SGI_MODE_EFT_LITERAL  AccuX exactly as listed (no renormalisation).
+ *   SGI_MODE_NAIVE        Eq.FINAL in plain binary64 (§4).
+ * Results are bit-identical to the CPU oracle's op sequence (oracle/eft_oracle.c) up to the sign
+ * of zero, independent of grid shape, stream or sharding.
+ *
+ * Layout (all arrays caller-owned; SoA planes with leading dimension ld >= n):
+ *   a[c*ld + i], b[c*ld + i]   endpoint coordinates, c = 0,1,2 = x,y,z        (float64)
+ *   z0[i]                      latitude plane height                         (float64)
+ *   out_xyz[(k*3 + c)*ld + i]  slot k = 0,1 of query i, coordinates c        (float64)
+ *   out_count[i]               0, 1, 2, or SGI_DEGENERATE                    (uint8)
+ * Slots hold the in-arc points in arc order (the first met travelling from a to b); unused
+ * slots are the canonical quiet NaN 0x7FF8000000000000.  out_xyz z-coordinates are bit copies
+ * of z0.  SGI_DEGENERATE (0xFF): n = 0 exactly (equal, antipodal or zero endpoints), or
+ * n_xy = 0 with z0 = 0 (arc on the equator, which is the latitude).  n_xy = 0 with z0 != 0
+ * gives count 0.  Inputs are assumed finite with nonzero component magnitudes in
+ * [2^-200, 2^200], so no error term of the EFT chain underflows or overflows (the analysis
+ * ignores the exponent range); NaN inputs give count 0.  No per-element condition
+ * fails a call.
+ *
+ * Errors: SGI_E_INVALID (nothing is launched) for a null pointer with n > 0, n < 0, ld < n,
+ * an unknown mode, or output arrays overlapping input arrays.  SGI_E_CUDA when a launch or
+ * copy fails; sgi_last_error() then returns the CUDA message (thread-local).  n == 0 returns
+ * SGI_OK without launching.
+ */
+#ifndef SGI_H
+#define SGI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SGI_ABI_VERSION 1
+#define SGI_DEGENERATE ((uint8_t)0xFF)
+
+typedef enum { SGI_MODE_NAIVE = 0, SGI_MODE_EFT = 1, SGI_MODE_EFT_LITERAL = 2 } sgi_mode;
+typedef enum { SGI_OK = 0, SGI_E_INVALID = 1, SGI_E_CUDA = 2 } sgi_status;
+
+/* Device entry point.  a, b, z0, out_xyz, out_count are CUDA device pointers.  Enqueues one
+ * kernel on `stream` (a cudaStream_t; NULL = legacy default stream) and returns without
+ * synchronising; performs no allocation and keeps no state, so it is thread-safe. */
+sgi_status sgi_intersect_arc_lat(const double* a, const double* b, const double* z0,
+                                 int64_t n, int64_t ld, double* out_xyz, uint8_t* out_count,
+                                 int mode, void* stream);
+
+/* Host-buffer entry point (the end-to-end path).  a, b, z0, out_xyz, out_count are HOST
+ * pointers in the layout above (page-locked memory lets the copies overlap; pageable works).
+ * d_work is a caller-owned device buffer of work_bytes >= sgi_host_workspace_bytes(chunk)
+ * bytes for some chunk >= 1; the batch is streamed through it in chunks, copies and kernels
+ * pipelined over `stream` and one internal stream.  Blocks until the results are on the host. */
+sgi_status sgi_intersect_arc_lat_host(const double* a, const double* b, const double* z0,
+                                      int64_t n, int64_t ld, double* out_xyz,
+                                      uint8_t* out_count, int mode, void* d_work,
+                                      size_t work_bytes, void* stream);
+
+/* Device bytes sgi_intersect_arc_lat_host needs for a given chunk length (two buffers). */
+size_t sgi_host_workspace_bytes(int64_t chunk);
+
+/* Histogram of out_count (device pointers): d_hist5[0..2] += number of queries with 0/1/2
+ * points, d_hist5[3] += number of SGI_DEGENERATE, d_hist5[4] += total points.  Accumulates
+ * into d_hist5 (the caller zeroes it); asynchronous on `stream`. */
+sgi_status sgi_count_histogram(const uint8_t* out_count, int64_t n,
+                               unsigned long long* d_hist5, void* stream);
+
+const char* sgi_status_str(sgi_status s);
+const char* sgi_last_error(void);
+int sgi_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SGI_H */

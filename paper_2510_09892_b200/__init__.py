@@ -1,0 +1,163 @@
+"""paper_2510_09892_b200 — B200-native batched arc/latitude intersections (arXiv 2510.09892).
+
+Thin ctypes binding over the C ABI of ``libsgi.so`` (include/sgi.h): argument marshalling only;
+every step of the path runs in the CUDA kernels of ``csrc/``.  There is no CPU fallback: if the
+library is missing or no CUDA device is present, calls raise.
+
+Public API (same names as the C ABI):
+    intersect_arc_lat(a, b, z0, mode="eft", out_xyz=None, out_count=None, n=None, stream=None)
+    intersect_arc_lat_host(a, b, z0, mode="eft", out_xyz=None, out_count=None, work=None, ...)
+    count_histogram(out_count, n=None, hist=None, stream=None)
+    host_workspace_bytes(chunk), abi_version(), status_str(code), last_error()
+Layout: a[3, ld], b[3, ld], z0[ld] float64; out_xyz[2, 3, ld] float64; out_count[ld] uint8.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+from ._build import LIB_PATH, build  # noqa: F401
+
+MODES = {"naive": 0, "eft": 1, "eft_literal": 2}
+DEGENERATE = 0xFF
+SGI_OK, SGI_E_INVALID, SGI_E_CUDA = 0, 1, 2
+
+_lib = None
+
+
+class SGIError(RuntimeError):
+    pass
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise SGIError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; "
+                           "g.build()'` (no CPU fallback exists)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i64 = ctypes.c_void_p, ctypes.c_int64
+        L.sgi_intersect_arc_lat.restype = ctypes.c_int
+        L.sgi_intersect_arc_lat.argtypes = [vp, vp, vp, i64, i64, vp, vp, ctypes.c_int, vp]
+        L.sgi_intersect_arc_lat_host.restype = ctypes.c_int
+        L.sgi_intersect_arc_lat_host.argtypes = [vp, vp, vp, i64, i64, vp, vp, ctypes.c_int, vp,
+                                                 ctypes.c_size_t, vp]
+        L.sgi_host_workspace_bytes.restype = ctypes.c_size_t
+        L.sgi_host_workspace_bytes.argtypes = [i64]
+        L.sgi_count_histogram.restype = ctypes.c_int
+        L.sgi_count_histogram.argtypes = [vp, i64, vp, vp]
+        L.sgi_status_str.restype = ctypes.c_char_p
+        L.sgi_status_str.argtypes = [ctypes.c_int]
+        L.sgi_last_error.restype = ctypes.c_char_p
+        L.sgi_last_error.argtypes = []
+        L.sgi_abi_version.restype = ctypes.c_int
+        L.sgi_abi_version.argtypes = []
+        _lib = L
+    return _lib
+
+
+def lib():
+    """The loaded libsgi.so (ctypes.CDLL)."""
+    return _load()
+
+
+def abi_version() -> int:
+    return _load().sgi_abi_version()
+
+
+def status_str(code: int) -> str:
+    return _load().sgi_status_str(code).decode()
+
+
+def last_error() -> str:
+    return _load().sgi_last_error().decode()
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != SGI_OK:
+        raise SGIError(f"{what}: {status_str(rc)}: {last_error()}")
+
+
+def _mode(mode) -> int:
+    return MODES[mode] if isinstance(mode, str) else int(mode)
+
+
+def _stream_ptr(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _cuda_f64(t, shape, name):
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64
+            and t.is_contiguous() and tuple(t.shape) == shape):
+        raise ValueError(f"{name} must be a contiguous CUDA float64 tensor of shape {shape}")
+
+
+def intersect_arc_lat(a, b, z0, mode="eft", out_xyz=None, out_count=None, n=None, stream=None):
+    """Device entry: torch CUDA tensors a[3, ld], b[3, ld], z0[ld] -> (out_xyz[2,3,ld], out_count[ld]).
+
+    Enqueued on `stream` (torch.cuda.Stream, default: current); does not synchronise."""
+    import torch
+    ld = z0.shape[0]
+    n = ld if n is None else n
+    _cuda_f64(a, (3, ld), "a")
+    _cuda_f64(b, (3, ld), "b")
+    _cuda_f64(z0, (ld,), "z0")
+    if out_xyz is None:
+        out_xyz = torch.empty((2, 3, ld), dtype=torch.float64, device=z0.device)
+    if out_count is None:
+        out_count = torch.empty(ld, dtype=torch.uint8, device=z0.device)
+    _cuda_f64(out_xyz, (2, 3, ld), "out_xyz")
+    if not (out_count.is_cuda and out_count.dtype == torch.uint8 and out_count.shape == (ld,)):
+        raise ValueError("out_count must be a CUDA uint8 tensor of shape (ld,)")
+    rc = _load().sgi_intersect_arc_lat(a.data_ptr(), b.data_ptr(), z0.data_ptr(), n, ld,
+                                       out_xyz.data_ptr(), out_count.data_ptr(), _mode(mode),
+                                       _stream_ptr(stream))
+    _check(rc, "sgi_intersect_arc_lat")
+    return out_xyz, out_count
+
+
+def host_workspace_bytes(chunk: int) -> int:
+    return int(_load().sgi_host_workspace_bytes(chunk))
+
+
+def intersect_arc_lat_host(a, b, z0, mode="eft", out_xyz=None, out_count=None, work=None,
+                           n=None, stream=None):
+    """Host-buffer entry (end to end): numpy or CPU torch arrays in, host arrays out.
+
+    `work` is a CUDA uint8 tensor used as the device workspace (default: a 64 Mi-arc chunk
+    buffer is allocated).  Pinned host memory lets the chunked copies overlap the kernels."""
+    import numpy as np
+    import torch
+
+    def ptr(x):
+        return x.data_ptr() if isinstance(x, torch.Tensor) else x.ctypes.data
+
+    ld = z0.shape[0]
+    n = ld if n is None else n
+    if out_xyz is None:
+        out_xyz = np.empty((2, 3, ld), np.float64)
+    if out_count is None:
+        out_count = np.empty(ld, np.uint8)
+    if work is None:
+        work = torch.empty(host_workspace_bytes(min(max(n, 1), 1 << 22)), dtype=torch.uint8,
+                           device="cuda")
+    rc = _load().sgi_intersect_arc_lat_host(ptr(a), ptr(b), ptr(z0), n, ld, ptr(out_xyz),
+                                            ptr(out_count), _mode(mode), work.data_ptr(),
+                                            work.numel(), _stream_ptr(stream))
+    _check(rc, "sgi_intersect_arc_lat_host")
+    return out_xyz, out_count
+
+
+def count_histogram(out_count, n=None, hist=None, stream=None):
+    """Device histogram [#0, #1, #2, #degenerate, #points] (int64 CUDA tensor, accumulated)."""
+    import torch
+    n = out_count.shape[0] if n is None else n
+    if hist is None:
+        hist = torch.zeros(5, dtype=torch.int64, device=out_count.device)
+    rc = _load().sgi_count_histogram(out_count.data_ptr(), n, hist.data_ptr(), _stream_ptr(stream))
+    _check(rc, "sgi_count_histogram")
+    return hist

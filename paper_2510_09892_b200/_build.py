@@ -1,0 +1,37 @@
+"""In-tree build of libsgi.so for sm_100a (nvcc cross-compiles without a GPU)."""
+from __future__ import annotations
+
+import glob
+import os
+import subprocess
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+LIB_PATH = os.path.join(PKG, "libsgi.so")
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
+              "-fmad=false",            # no contraction: each fl() is one rounding
+              "-Xptxas", "-v", "-Xcompiler", "-fPIC", "-shared", "-std=c++17"]
+
+
+def sources() -> list[str]:
+    return sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu")) +
+                  glob.glob(os.path.join(PKG, "csrc", "*.cuh")) +
+                  [os.path.join(ROOT, "include", "sgi.h")])
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile csrc/*.cu into paper_2510_09892_b200/libsgi.so if any source is newer."""
+    srcs = sources()
+    if (not force and os.path.exists(LIB_PATH)
+            and all(os.path.getmtime(LIB_PATH) >= os.path.getmtime(s) for s in srcs)):
+        return LIB_PATH
+    cu = [s for s in srcs if s.endswith(".cu")]
+    cmd = ["nvcc", *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB_PATH, *cu]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
+    with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
+        f.write(res.stderr)
+    if verbose:
+        print(res.stderr)
+    return LIB_PATH

@@ -1,0 +1,103 @@
+"""The C ABI (include/sgi.h) without a GPU: the library loads, exports every declared symbol,
+and rejects invalid arguments before touching CUDA."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2510_09892_b200 as sgi
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    sgi.build()
+    return sgi.lib()
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "sgi.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(sgi_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    assert declared_symbols() == sorted([
+        "sgi_intersect_arc_lat", "sgi_intersect_arc_lat_host", "sgi_host_workspace_bytes",
+        "sgi_count_histogram", "sgi_status_str", "sgi_last_error", "sgi_abi_version"])
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+
+
+def test_no_torch_in_signatures():
+    src = open(os.path.join(ROOT, "include", "sgi.h")).read()
+    assert "torch" not in src.lower().replace("pytorch", "") and "at::" not in src
+
+
+def test_version_and_status_strings(lib):
+    assert sgi.abi_version() == 1
+    assert [sgi.status_str(c) for c in (0, 1, 2)] == ["SGI_OK", "SGI_E_INVALID", "SGI_E_CUDA"]
+
+
+def test_workspace_bytes(lib):
+    assert sgi.host_workspace_bytes(0) == 0
+    assert sgi.host_workspace_bytes(1) == 2 * (13 * 256 + 256)
+    assert sgi.host_workspace_bytes(1 << 20) == 2 * (13 * (8 << 20) + (1 << 20))
+
+
+def _call(lib, a, b, z, n, ld, out, cnt, mode):
+    return lib.sgi_intersect_arc_lat(a, b, z, n, ld, out, cnt, mode, None)
+
+
+def test_invalid_arguments_rejected_without_launch(lib):
+    n = 64
+    a = np.zeros((3, n)); b = np.zeros((3, n)); z = np.zeros(n)
+    out = np.zeros((2, 3, n)); cnt = np.zeros(n, np.uint8)
+    P = lambda x: x.ctypes.data  # noqa: E731
+    assert _call(lib, P(a), P(b), P(z), -1, n, P(out), P(cnt), 1) == sgi.SGI_E_INVALID
+    assert _call(lib, P(a), P(b), P(z), n, n - 1, P(out), P(cnt), 1) == sgi.SGI_E_INVALID
+    assert _call(lib, P(a), P(b), P(z), n, n, P(out), P(cnt), 3) == sgi.SGI_E_INVALID
+    assert _call(lib, P(a), P(b), P(z), n, n, P(out), P(cnt), -1) == sgi.SGI_E_INVALID
+    assert _call(lib, None, P(b), P(z), n, n, P(out), P(cnt), 1) == sgi.SGI_E_INVALID
+    assert "null" in sgi.last_error()
+    # outputs aliasing inputs
+    assert _call(lib, P(a), P(b), P(z), n, n, P(a), P(cnt), 1) == sgi.SGI_E_INVALID
+    assert "overlap" in sgi.last_error()
+    assert _call(lib, P(a), P(b), P(z), n, n, P(out), P(out), 1) == sgi.SGI_E_INVALID
+    # n == 0 is a no-op, even with null pointers
+    assert _call(lib, None, None, None, 0, 0, None, None, 1) == sgi.SGI_OK
+    assert lib.sgi_count_histogram(None, -1, None, None) == sgi.SGI_E_INVALID
+    assert lib.sgi_count_histogram(None, 0, None, None) == sgi.SGI_OK
+
+
+def test_host_entry_validates_workspace(lib):
+    n = 16
+    a = np.zeros((3, n)); b = np.zeros((3, n)); z = np.zeros(n)
+    out = np.zeros((2, 3, n)); cnt = np.zeros(n, np.uint8)
+    P = lambda x: x.ctypes.data  # noqa: E731
+    rc = lib.sgi_intersect_arc_lat_host(P(a), P(b), P(z), n, n, P(out), P(cnt), 1, None, 0, None)
+    assert rc == sgi.SGI_E_INVALID
+
+
+def test_product_package_does_not_import_oracle():
+    """The product path never routes through the oracle (no CPU fallback)."""
+    pkg = os.path.join(ROOT, "paper_2510_09892_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in text and "from oracle" not in text, f
+                assert "eft_oracle" not in text, f
+
+
+def test_missing_library_fails_loudly(tmp_path, monkeypatch):
+    monkeypatch.setattr(sgi, "_lib", None)
+    monkeypatch.setattr(sgi, "LIB_PATH", str(tmp_path / "libsgi.so"))
+    with pytest.raises(sgi.SGIError):
+        sgi.abi_version()

@@ -1,0 +1,309 @@
+"""GPU parity: the CUDA path (through the C ABI) against oracle (a) element by element and
+against oracle (b) on samples, on every BASELINE.json config, plus edge cases.
+
+Parity bar: counts bit-exact; points bitwise equal to oracle (a) up to the sign
+of zero (IEEE ==, NaN == NaN); EFT points within err_u <= 3 of oracle (b) (Eq.BOUND,
+P:897-913).  Sizes: C1 in full; C2, C3 in full (2^24, the bench's launch configuration);
+C4 in full (~6.0 M pairs); C5 (2^30) on a deterministic sample of global indices generated on
+the device in the bench's launch configuration.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import sgi_inputs
+from oracle import exact
+
+torch = pytest.importorskip("torch")
+import paper_2510_09892_b200 as sgi  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+MODES = [("eft", oracle.MODE_EFT), ("eft_literal", oracle.MODE_EFT_LITERAL),
+         ("naive", oracle.MODE_NAIVE)]
+NTHREADS = 16
+
+
+def same(x, y):
+    return (x == y) | (np.isnan(x) & np.isnan(y))
+
+
+def run_gpu(a, b, z0, mode, n=None):
+    da, db, dz = (torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (a, b, z0))
+    out, cnt = sgi.intersect_arc_lat(da, db, dz, mode=mode, n=n)
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), cnt.cpu().numpy()
+
+
+def assert_parity(got, gcnt, ref, rcnt, n=None):
+    n = len(rcnt) if n is None else n
+    assert np.array_equal(gcnt[:n], rcnt[:n]), int((gcnt[:n] != rcnt[:n]).sum())
+    ok = same(got[..., :n], ref[..., :n])
+    assert ok.all(), f"{int((~ok).sum())} coordinates differ"
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _build():
+    sgi.build()
+    sgi_inputs.build(device=True)
+
+
+# ------------------------------------------------------------------ device generator == host
+@pytest.mark.parametrize("config", [1, 2, 3, 5])
+def test_device_generator_matches_host(config):
+    n = 100_003
+    a, b, z = sgi_inputs.generate_host(config, n, offset=12345)
+    da = torch.empty((3, n), dtype=torch.float64, device="cuda")
+    db = torch.empty_like(da)
+    dz = torch.empty(n, dtype=torch.float64, device="cuda")
+    sgi_inputs.generate_device(config, n, da, db, dz, offset=12345)
+    torch.cuda.synchronize()
+    assert np.array_equal(da.cpu().numpy(), a)
+    assert np.array_equal(db.cpu().numpy(), b)
+    assert np.array_equal(dz.cpu().numpy(), z)
+
+
+# ------------------------------------------------------------------------------ C1 in full
+@pytest.mark.parametrize("mode,omode", MODES)
+def test_c1_parity_all_modes(mode, omode):
+    a, b, z0 = sgi_inputs.generate_host(1, sgi_inputs.CONFIG_SIZES[1])
+    got, gcnt = run_gpu(a, b, z0, mode)
+    ref, rcnt = oracle.intersect(omode, a, b, z0, nthreads=NTHREADS)
+    assert_parity(got, gcnt, ref, rcnt)
+
+
+def test_c1_eft_against_exact_oracle():
+    a, b, z0 = sgi_inputs.generate_host(1, sgi_inputs.CONFIG_SIZES[1])
+    got, gcnt = run_gpu(a, b, z0, "eft")
+    worst = 0.0
+    for i in range(len(z0)):
+        ex = exact.exact_query(a[:, i], b[:, i], z0[i])
+        assert ex.count == gcnt[i]
+        for k in range(ex.count if ex.count != exact.DEGENERATE else 0):
+            worst = max(worst, exact.err_u((got[k, 0, i], got[k, 1, i]), ex.points[k], z0[i]))
+    assert worst <= 3.0
+
+
+# -------------------------------------------------------- C2, C3 at full size (2^24 each)
+def _device_config(config, n):
+    da = torch.empty((3, n), dtype=torch.float64, device="cuda")
+    db = torch.empty_like(da)
+    dz = torch.empty(n, dtype=torch.float64, device="cuda")
+    sgi_inputs.generate_device(config, n, da, db, dz)
+    return da, db, dz
+
+
+@pytest.mark.parametrize("config", [2, 3])
+@pytest.mark.parametrize("mode,omode", MODES)
+def test_full_size_parity(config, mode, omode):
+    n = sgi_inputs.CONFIG_SIZES[config]
+    da, db, dz = _device_config(config, n)
+    out, cnt = sgi.intersect_arc_lat(da, db, dz, mode=mode)
+    torch.cuda.synchronize()
+    a, b, z0 = da.cpu().numpy(), db.cpu().numpy(), dz.cpu().numpy()
+    ref, rcnt = oracle.intersect(omode, a, b, z0, nthreads=NTHREADS)
+    assert_parity(out.cpu().numpy(), cnt.cpu().numpy(), ref, rcnt)
+
+
+@pytest.mark.parametrize("config", [2, 3])
+def test_full_size_eft_sampled_exact(config):
+    n = sgi_inputs.CONFIG_SIZES[config]
+    da, db, dz = _device_config(config, n)
+    out, cnt = sgi.intersect_arc_lat(da, db, dz, mode="eft")
+    torch.cuda.synchronize()
+    idx = np.random.default_rng(config).choice(n, 1500, replace=False)
+    a, b, z0 = da[:, idx].cpu().numpy(), db[:, idx].cpu().numpy(), dz[idx].cpu().numpy()
+    got, gcnt = out[:, :, idx].cpu().numpy(), cnt[idx].cpu().numpy()
+    worst, bad = 0.0, []
+    for j in range(len(idx)):
+        ex = exact.exact_query(a[:, j], b[:, j], z0[j])
+        if ex.count != gcnt[j]:
+            bad.append(min(ex.margins))          # endpoint-on-latitude ties (R7)
+            continue
+        for k in range(ex.count if ex.count != exact.DEGENERATE else 0):
+            worst = max(worst, exact.err_u((got[k, 0, j], got[k, 1, j]), ex.points[k], z0[j]))
+    assert worst <= 3.0
+    assert all(m < 4 * 2.0 ** -53 for m in bad) and len(bad) <= 15
+
+
+# ------------------------------------------------------------------------- C4 in full
+def test_c4_full_parity():
+    a, b, z0, _ = sgi_inputs.c4_pairs(1024, 1800)
+    got, gcnt = run_gpu(a, b, z0, "eft")
+    ref, rcnt = oracle.intersect(oracle.MODE_EFT, a, b, z0, nthreads=NTHREADS)
+    assert_parity(got, gcnt, ref, rcnt)
+    idx = np.random.default_rng(44).choice(len(z0), 1000, replace=False)
+    for i in idx:
+        ex = exact.exact_query(a[:, i], b[:, i], z0[i])
+        assert ex.count == gcnt[i]
+        for k in range(ex.count if ex.count != exact.DEGENERATE else 0):
+            assert exact.err_u((got[k, 0, i], got[k, 1, i]), ex.points[k], z0[i]) <= 3.0
+
+
+# ------------------------------------------------- C5 (2^30) sampled, generated on the device
+def test_c5_full_size_sampled():
+    n = sgi_inputs.CONFIG_SIZES[5]
+    free, _ = torch.cuda.mem_get_info()
+    if free < n * 110:
+        pytest.skip("needs ~113 GB free HBM")
+    da, db, dz = _device_config(5, n)
+    out, cnt = sgi.intersect_arc_lat(da, db, dz, mode="eft")
+    hist = sgi.count_histogram(cnt)
+    torch.cuda.synchronize()
+    idx = np.unique(np.concatenate([np.arange(0, n, 4096),
+                                    np.random.default_rng(5).choice(n, 4096), [n - 1]]))
+    ti = torch.from_numpy(idx).cuda()
+    got = out[:, :, ti].cpu().numpy()
+    gcnt = cnt[ti].cpu().numpy()
+    a, b, z0 = da[:, ti].cpu().numpy(), db[:, ti].cpu().numpy(), dz[ti].cpu().numpy()
+    del da, db, dz, out, cnt
+    ref, rcnt = oracle.intersect(oracle.MODE_EFT, a, b, z0, nthreads=NTHREADS)
+    assert_parity(got, gcnt, ref, rcnt)
+    # the sample really is what the host generator makes for those global indices
+    for j in (0, len(idx) // 2, len(idx) - 1):
+        ha, hb, hz = sgi_inputs.generate_host(5, 1, offset=int(idx[j]))
+        assert np.array_equal(ha[:, 0], a[:, j]) and hz[0] == z0[j]
+    h = hist.cpu().numpy()
+    assert h[:4].sum() == n and h[4] == h[1] + 2 * h[2]
+    assert h[0] > 0 and h[1] > 0 and h[2] > 0       # mixed 0/1/2 by construction (config 5)
+    worst = 0.0
+    for j in range(0, len(idx), 4):
+        ex = exact.exact_query(a[:, j], b[:, j], z0[j])
+        assert ex.count == gcnt[j]
+        for k in range(ex.count if ex.count != exact.DEGENERATE else 0):
+            worst = max(worst, exact.err_u((got[k, 0, j], got[k, 1, j]), ex.points[k], z0[j]))
+    assert worst <= 3.0
+
+
+# ---------------------------------------------------------------------------- edge cases
+@pytest.mark.parametrize("n", [1, 31, 255, 257, 1000, 148 * 256 * 4 + 77])
+def test_ragged_sizes_and_padding(n):
+    ld = n + 13
+    a, b, z0 = sgi_inputs.generate_host(5, n, ld=ld)
+    a[:, n:] = 7.0; b[:, n:] = 7.0; z0[n:] = 0.5               # padding must not be read as data
+    da, db, dz = (torch.from_numpy(x).cuda() for x in (a, b, z0))
+    out = torch.full((2, 3, ld), -123.0, dtype=torch.float64, device="cuda")
+    cnt = torch.full((ld,), 77, dtype=torch.uint8, device="cuda")
+    sgi.intersect_arc_lat(da, db, dz, mode="eft", out_xyz=out, out_count=cnt, n=n)
+    torch.cuda.synchronize()
+    got, gcnt = out.cpu().numpy(), cnt.cpu().numpy()
+    ref, rcnt = oracle.intersect(oracle.MODE_EFT, a, b, z0, n=n)
+    assert_parity(got, gcnt, ref, rcnt, n=n)
+    assert (got[..., n:] == -123.0).all() and (gcnt[n:] == 77).all()
+
+
+def test_empty_batch_is_a_noop():
+    z = torch.empty(0, dtype=torch.float64, device="cuda")
+    out, cnt = sgi.intersect_arc_lat(torch.empty((3, 0), dtype=torch.float64, device="cuda"),
+                                     torch.empty((3, 0), dtype=torch.float64, device="cuda"), z)
+    assert out.shape == (2, 3, 0) and cnt.shape == (0,)
+
+
+def degenerate_and_special():
+    """Hand-made edge inputs: degenerate arcs, exact zeros, poles, huge/tiny scales, NaN."""
+    rows = [
+        ((1, 0, 0), (0, 0, 1), 0.5), ((1, 0, 0), (0, 0, 1), 0.0), ((1, 0, 0), (0, 0, 1), 1.0),
+        ((1, 0, 0), (0, 0, 1), 1.0000000000000009), ((1, 0, 0), (0, 1, 0), 0.0),
+        ((1, 0, 0), (0, 1, 0), 0.5), ((0.6, 0, 0.8), (0.6, 0, 0.8), 0.5),
+        ((1, 0, 0), (-1, 0, 0), 0.0), ((0, 0, 0), (1, 0, 0), 0.3), ((0, 0, 1), (0, 0, -1), 0.0),
+        ((1, 0, 1), (-1, 0, 1), 0.75), ((1, 0, -1), (-1, 0, -1), -0.75),
+        ((2.0 ** 150, 0, 2.0 ** 150), (-(2.0 ** 150), 0, 2.0 ** 150), 0.75),
+        ((2.0 ** -150, 0, 2.0 ** -150), (-(2.0 ** -150), 0, 2.0 ** -150), 0.75),
+        ((1, 0, 0), (0, 0, 1), float("nan")), ((float("nan"), 0, 0), (0, 0, 1), 0.5),
+        ((0, 0, 1), (1, 0, 0), -0.0), ((1, 1e-300, 0), (1, -1e-300, 0), 0.0),
+        ((0.3, 0.4, 0.5), (0.3, 0.4, 0.5000000000000001), 0.5),
+    ]
+    a = np.array([r[0] for r in rows], float).T.copy()
+    b = np.array([r[1] for r in rows], float).T.copy()
+    z = np.array([r[2] for r in rows], float)
+    return a, b, z
+
+
+@pytest.mark.parametrize("mode,omode", MODES)
+def test_edge_inputs(mode, omode):
+    a, b, z0 = degenerate_and_special()
+    got, gcnt = run_gpu(a, b, z0, mode)
+    ref, rcnt = oracle.intersect(omode, a, b, z0)
+    assert_parity(got, gcnt, ref, rcnt)
+    assert gcnt[4] == 0xFF and gcnt[6] == 0xFF and gcnt[7] == 0xFF and gcnt[8] == 0xFF
+    assert gcnt[14] == 0 and gcnt[15] == 0                     # NaN inputs: no points
+
+
+def test_output_layout_and_canonical_nan():
+    a, b, z0 = sgi_inputs.generate_host(5, 4096)
+    got, gcnt = run_gpu(a, b, z0, "eft")
+    bits = got.view(np.uint64)
+    for k in range(2):
+        used = (gcnt != 0xFF) & (gcnt > k)
+        assert np.array_equal(got[k, 2, used], z0[used])                   # P_z = z0 bitwise
+        assert (bits[k, :, ~used] == 0x7FF8000000000000).all()            # canonical qNaN
+
+
+def test_power_of_two_scaling_gpu():
+    a, b, z0 = sgi_inputs.generate_host(3, 30000)
+    base, bc = run_gpu(a, b, z0, "eft")
+    for k in (-30, 30):
+        got, gc = run_gpu(a * 2.0 ** k, b, z0, "eft")
+        assert np.array_equal(gc, bc) and same(got, base).all()
+
+
+# --------------------------------------------------------- host entry, streams, determinism
+@pytest.mark.parametrize("mode", ["eft", "naive"])
+def test_host_entry_matches_device_entry(mode):
+    n = 1_000_003
+    a, b, z0 = sgi_inputs.generate_host(5, n)
+    dev, dcnt = run_gpu(a, b, z0, mode)
+    pa, pb, pz = (torch.from_numpy(x).pin_memory() for x in (a, b, z0))
+    out = torch.empty((2, 3, n), dtype=torch.float64).pin_memory()
+    cnt = torch.empty(n, dtype=torch.uint8).pin_memory()
+    work = torch.empty(sgi.host_workspace_bytes(100_000), dtype=torch.uint8, device="cuda")
+    sgi.intersect_arc_lat_host(pa, pb, pz, mode=mode, out_xyz=out, out_count=cnt, work=work)
+    assert np.array_equal(cnt.numpy(), dcnt) and same(out.numpy(), dev).all()
+    # pageable numpy buffers work too
+    o2, c2 = sgi.intersect_arc_lat_host(a, b, z0, mode=mode, work=work)
+    assert np.array_equal(c2, dcnt) and same(o2, dev).all()
+
+
+def test_side_stream_and_repeatability():
+    n = 1 << 20
+    da, db, dz = _device_config(5, n)
+    out1, cnt1 = sgi.intersect_arc_lat(da, db, dz, mode="eft")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        out2, cnt2 = sgi.intersect_arc_lat(da, db, dz, mode="eft", stream=s)
+    torch.cuda.synchronize()
+    assert torch.equal(cnt1, cnt2)
+    assert torch.equal(out1.view(torch.int64), out2.view(torch.int64))   # bitwise
+
+
+def test_sharding_is_rank_invariant():
+    """R = 1, 2, 4, 8 shards (generated by global index) concatenate to the R = 1 result."""
+    n = 1 << 20
+    da, db, dz = _device_config(5, n)
+    ref, rcnt = sgi.intersect_arc_lat(da, db, dz, mode="eft")
+    hist_ref = sgi.count_histogram(rcnt)
+    for R in (2, 4, 8):
+        hist = torch.zeros(5, dtype=torch.int64, device="cuda")
+        for r in range(R):
+            lo, hi = r * n // R, (r + 1) * n // R
+            m = hi - lo
+            sa = torch.empty((3, m), dtype=torch.float64, device="cuda")
+            sb = torch.empty_like(sa)
+            sz = torch.empty(m, dtype=torch.float64, device="cuda")
+            sgi_inputs.generate_device(5, m, sa, sb, sz, offset=lo)
+            o, c = sgi.intersect_arc_lat(sa, sb, sz, mode="eft")
+            sgi.count_histogram(c, hist=hist)
+            assert torch.equal(c, rcnt[lo:hi])
+            assert torch.equal(o.view(torch.int64), ref[:, :, lo:hi].contiguous().view(torch.int64))
+        assert torch.equal(hist, hist_ref)
+
+
+def test_histogram_matches_bincount():
+    a, b, z0 = sgi_inputs.generate_host(5, 200_000)
+    da, db, dz = (torch.from_numpy(x).cuda() for x in (a, b, z0))
+    _, cnt = sgi.intersect_arc_lat(da, db, dz, mode="eft")
+    hist = sgi.count_histogram(cnt).cpu().numpy()
+    c = cnt.cpu().numpy()
+    assert hist.tolist() == [int((c == 0).sum()), int((c == 1).sum()), int((c == 2).sum()),
+                             int((c == 0xFF).sum()), int((c == 1).sum() + 2 * (c == 2).sum())]
