@@ -35,3 +35,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         print(res.stderr)
     return LIB_PATH
+
+
+DEVTEST_SRC = os.path.join(ROOT, "tests", "native", "devtests.cu")
+DEVTEST_LIB = os.path.join(ROOT, "tests", "native", "libsgi_devtest.so")
+
+
+def build_devtests(force: bool = False) -> str:
+    """Test-only library: device unit tests of the EFT primitives (tests/native)."""
+    deps = [DEVTEST_SRC] + sources()
+    if (not force and os.path.exists(DEVTEST_LIB)
+            and all(os.path.getmtime(DEVTEST_LIB) >= os.path.getmtime(s) for s in deps)):
+        return DEVTEST_LIB
+    cmd = ["nvcc", *[f for f in NVCC_FLAGS if f not in ("-Xptxas", "-v")], "-o", DEVTEST_LIB,
+           DEVTEST_SRC]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
+    return DEVTEST_LIB

@@ -1,0 +1,80 @@
+// tests/native/devtests.cu — device unit tests of the EFT primitives in csrc/sgi_eft.cuh.
+// Test-only library (libsgi_devtest.so); checks the value-preserving rewrites of DESIGN.md §5
+// against the reference formulations ON THE DEVICE, bit for bit, over counter-based random
+// inputs with adversarial exponent spreads, cancellations, zeros and guard-boundary values:
+//   two_sum (ordered FastTwoSum)  vs  two_sum_knuth (6-op TwoSum)     values, and e == a+b-s
+//   div_fast with a shared div_recip  vs  __ddiv_rn                   (when its guard passes)
+//   sqrt_fast                         vs  __dsqrt_rn                  (when its guard passes)
+// and counts how often each guard fails (the Exact recomputation rate).
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../paper_2510_09892_b200/csrc/sgi_eft.cuh"
+
+__device__ __forceinline__ uint64_t mix(uint64_t x) {
+  x ^= x >> 33; x *= 0xff51afd7ed558ccdull; x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ull; x ^= x >> 33;
+  return x;
+}
+
+// random double with exponent in [emin, emax], random sign; some specials
+__device__ double rnd(uint64_t key, int emin, int emax) {
+  uint64_t r = mix(key);
+  uint64_t sel = r & 63;
+  if (sel == 0) return 0.0;
+  if (sel == 1) return -0.0;
+  uint64_t mant = mix(r + 0x9e3779b97f4a7c15ull) & 0xFFFFFFFFFFFFFull;
+  int e = emin + (int)((r >> 8) % (uint64_t)(emax - emin + 1));
+  uint64_t sign = (r >> 7) & 1;
+  uint64_t bits = (sign << 63) | ((uint64_t)(e + 1023) << 52) | mant;
+  return __longlong_as_double((long long)bits);
+}
+
+__device__ bool same_bits_or_zero(double a, double b) {
+  return __double_as_longlong(a) == __double_as_longlong(b) || (a == 0.0 && b == 0.0);
+}
+
+// out[0]: two_sum value mismatches; out[1]: zero-sign-only differences; out[2]: exactness
+// failures (e != a + b - s checked with a second TwoSum); out[3]: div mismatches (guard ok);
+// out[4]: div guard failures; out[5]: sqrt mismatches (guard ok); out[6]: sqrt guard failures
+extern "C" __global__ void devtest_kernel(uint64_t seed, int64_t n, unsigned long long* out) {
+  unsigned long long c[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k = seed * 0x100000001b3ull + (uint64_t)i * 8;
+    double a = rnd(k, -200, 200);
+    double b;
+    uint64_t mode = mix(k + 1) % 4;
+    if (mode == 0) b = rnd(k + 2, -200, 200);
+    else if (mode == 1) b = -a * (1.0 + (double)((int)(mix(k + 3) % 9) - 4) * 1.1102230246251565e-16);
+    else if (mode == 2) b = rnd(k + 2, -60, 60) * a;
+    else b = a * 0.5 + rnd(k + 2, -120, -40);
+    sgi::dd x = sgi::two_sum(a, b), y = sgi::two_sum_knuth(a, b);
+    if (x.hi != y.hi || x.lo != y.lo) c[0]++;
+    else if (__double_as_longlong(x.lo) != __double_as_longlong(y.lo)) c[1]++;
+    // exactness: s + e == a + b  <=>  TwoSum(s, e) reproduces (s, e) and a - s + b == e exactly
+    sgi::dd z = sgi::two_sum_knuth(x.hi, x.lo);
+    if (z.hi != x.hi || z.lo != x.lo) c[2]++;
+    // division with a shared reciprocal (numerators spread over many magnitudes, some tiny)
+    double den = fabs(rnd(k + 4, -100, 100)) + 1e-300;
+    double y0 = sgi::div_recip(den);
+    for (int j = 0; j < 4; ++j) {
+      double num = rnd(k + 5 + j, (j == 3) ? -1070 : -200, 200);
+      bool ok = true;
+      double q = sgi::div_fast(num, den, y0, ok);
+      if (!ok) { c[4]++; continue; }
+      if (!same_bits_or_zero(q, __ddiv_rn(num, den))) c[3]++;
+    }
+    double sx = fabs(rnd(k + 9, (mode == 3) ? -1074 : -300, 300));
+    bool oks = true;
+    double r = sgi::sqrt_fast(sx, oks);
+    if (!oks) c[6]++;
+    else if (!same_bits_or_zero(r, __dsqrt_rn(sx))) c[5]++;
+  }
+  for (int j = 0; j < 7; ++j)
+    if (c[j]) atomicAdd(out + j, c[j]);
+}
+
+extern "C" int sgi_devtest(uint64_t seed, int64_t n, unsigned long long* d_out) {
+  cudaMemset(d_out, 0, 7 * sizeof(unsigned long long));
+  devtest_kernel<<<148 * 8, 256>>>(seed, n, d_out);
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : 1;
+}
