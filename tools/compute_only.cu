@@ -1,0 +1,49 @@
+// Compute-only throughput of the per-query device code (tools, not product): each thread runs
+// the EFT query on register-resident synthetic arcs (perturbed each iteration so nothing is
+// hoisted), folding the outputs into a checksum; no HBM traffic.  Prints ns per query for a
+// few occupancies, to separate FP64/issue efficiency from memory effects.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false -I include -o tools/compute_only tools/compute_only.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+#include "../paper_2510_09892_b200/csrc/sgi_query.cuh"
+
+template <int MODE, int MINB>
+__global__ void __launch_bounds__(256, MINB) bench(int iters, double* sink) {
+  double x1 = 0.6 + threadIdx.x * 1e-5, y1 = 0.3, z1 = 0.74, x2 = 0.59, y2 = 0.31 + blockIdx.x * 1e-7;
+  double z2 = 0.745, z0 = 0.742;
+  double acc = 0.0;
+  for (int it = 0; it < iters; ++it) {
+    sgi::RegIn in = {{x1, y1, z1, x2, y2, z2}};
+    sgi::QueryOut o;
+    bool ok = sgi::query_fast<MODE>(in, z0, o);
+    acc += o.p0x + (ok ? 0.0 : 1.0) + o.count;
+    x1 = __dadd_rn(x1, 1e-9); y2 = __dadd_rn(y2, 1e-9);
+  }
+  if (acc == 12345.0) sink[0] = acc;
+}
+
+template <int MODE, int MINB>
+void run(const char* name, int blocks_per_sm) {
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  double* sink; cudaMalloc(&sink, 8);
+  int iters = 2000;
+  dim3 grid(sms * blocks_per_sm);
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  bench<MODE, MINB><<<grid, 256>>>(10, sink);
+  cudaEventRecord(a);
+  bench<MODE, MINB><<<grid, 256>>>(iters, sink);
+  cudaEventRecord(b); cudaEventSynchronize(b);
+  float ms; cudaEventElapsedTime(&ms, a, b);
+  double q = (double)grid.x * 256 * iters;
+  printf("%-22s blocks/SM=%d  %.4f ns/query  -> 2^24 queries in %.4f ms  (%s)\n", name,
+         blocks_per_sm, ms * 1e6 / q, ms * 1e6 / q * 16777216 / 1e6, cudaGetErrorString(cudaGetLastError()));
+}
+
+int main() {
+  run<sgi::MODE_EFT, 1>("eft", 1);
+  run<sgi::MODE_EFT, 1>("eft", 2);
+  run<sgi::MODE_EFT, 1>("eft", 3);
+  run<sgi::MODE_EFT, 4>("eft minb4", 4);
+  run<sgi::MODE_NAIVE, 1>("naive", 3);
+  return 0;
+}

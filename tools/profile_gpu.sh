@@ -14,7 +14,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 echo "launch list rc=$?"
 for MODE in eft naive; do
   python bench.py --mode $MODE --steps 3 --warmup 3 --e2e-steps 0 --no-cpu-baseline > $OUT/${TAG}_${MODE}_plain2.log 2>&1 &&
-  ncu --set full --clock-control none --import-source on -k regex:sgi_intersect_kernel -s 4 -c 1 \
+  ncu --set full --clock-control none --import-source on -k regex:sgi_intersect -s 4 -c 1 \
       -o $OUT/${TAG}_${MODE} python bench.py --mode $MODE --steps 3 --warmup 3 --e2e-steps 0 \
       --no-cpu-baseline > $OUT/${TAG}_${MODE}_ncu.log 2>&1
   echo "full capture $MODE rc=$?"

@@ -17,16 +17,19 @@ OUT = os.path.join(ROOT, "build", "variants")
 
 VARIANTS = {
     "base": {},
-    "t128": {"SGI_THREADS": 128},
-    "t160": {"SGI_THREADS": 160},
-    "t192": {"SGI_THREADS": 192},
-    "minb3": {"SGI_MINB": 3},
-    "t128_minb6": {"SGI_THREADS": 128, "SGI_MINB": 6},
-    "knuth": {"SGI_TS_KNUTH": 1},
-    "knuth_minb3": {"SGI_TS_KNUTH": 1, "SGI_MINB": 3},
-    "grid8": {"SGI_GRID_MULT": 8},
-    "t128_grid8": {"SGI_THREADS": 128, "SGI_GRID_MULT": 8},
-    "ilp2_minb1": {"SGI_ILP": 2, "SGI_MINB": 1},
+    "ldg": {'SGI_USE_TMA': 0},
+    "e256_s2": {'SGI_EFT_THREADS': 256, 'SGI_EFT_STAGES': 2, 'SGI_NAIVE_THREADS': 256, 'SGI_NAIVE_STAGES': 2},
+    "e256_s3": {'SGI_EFT_THREADS': 256, 'SGI_EFT_STAGES': 3, 'SGI_NAIVE_THREADS': 256, 'SGI_NAIVE_STAGES': 3},
+    "e384_s2": {'SGI_EFT_THREADS': 384, 'SGI_EFT_STAGES': 2, 'SGI_NAIVE_THREADS': 256, 'SGI_NAIVE_STAGES': 2},
+    "e384_s3": {'SGI_EFT_THREADS': 384, 'SGI_EFT_STAGES': 3, 'SGI_NAIVE_THREADS': 256, 'SGI_NAIVE_STAGES': 3},
+    "e512_s2": {'SGI_EFT_THREADS': 512, 'SGI_EFT_STAGES': 2, 'SGI_NAIVE_THREADS': 512, 'SGI_NAIVE_STAGES': 3},
+    "e512_s3": {'SGI_EFT_THREADS': 512, 'SGI_EFT_STAGES': 3, 'SGI_NAIVE_THREADS': 512, 'SGI_NAIVE_STAGES': 4},
+    "e640_s2": {'SGI_EFT_THREADS': 640, 'SGI_EFT_STAGES': 2, 'SGI_NAIVE_THREADS': 512, 'SGI_NAIVE_STAGES': 2},
+    "e640_s3": {'SGI_EFT_THREADS': 640, 'SGI_EFT_STAGES': 3, 'SGI_NAIVE_THREADS': 512, 'SGI_NAIVE_STAGES': 3},
+    "e768_s2": {'SGI_EFT_THREADS': 768, 'SGI_EFT_STAGES': 2, 'SGI_NAIVE_THREADS': 128, 'SGI_NAIVE_STAGES': 2},
+    "e768_s3": {'SGI_EFT_THREADS': 768, 'SGI_EFT_STAGES': 3, 'SGI_NAIVE_THREADS': 128, 'SGI_NAIVE_STAGES': 3},
+    "e1024_s2": {'SGI_EFT_THREADS': 1024, 'SGI_EFT_STAGES': 2, 'SGI_NAIVE_THREADS': 256, 'SGI_NAIVE_STAGES': 3},
+    "e1024_s3": {'SGI_EFT_THREADS': 1024, 'SGI_EFT_STAGES': 3, 'SGI_NAIVE_THREADS': 256, 'SGI_NAIVE_STAGES': 4},
 }
 
 
@@ -44,47 +47,69 @@ def build():
         print(name, regs[:6])
 
 
-def time_all(n):
+def time_all(n, rounds=7, reps=20):
+    """Interleaved timing: every round times every (variant, mode) once, so clock drift hits
+    all variants alike; reports the median over rounds and the SM clock seen (NVML)."""
+    import statistics
     import torch
     import sgi_inputs
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(0)
+        clock = lambda: pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)  # noqa: E731
+    except Exception:
+        clock = lambda: -1  # noqa: E731
     dev = torch.device("cuda", 0)
     a = torch.empty((3, n), dtype=torch.float64, device=dev)
     b = torch.empty_like(a)
     z0 = torch.empty(n, dtype=torch.float64, device=dev)
     sgi_inputs.generate_device(2, n, a, b, z0)
-    ref = {}
-    rows = []
+    out = torch.empty((2, 3, n), dtype=torch.float64, device=dev)
+    cnt = torch.empty(n, dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream()
+    fns = {}
     for name in VARIANTS:
         L = ctypes.CDLL(os.path.join(OUT, f"libsgi_{name}.so"))
         f = L.sgi_intersect_arc_lat
         f.restype = ctypes.c_int
         f.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int64] * 2 + [ctypes.c_void_p] * 2 + \
             [ctypes.c_int, ctypes.c_void_p]
-        for mode in (1, 0, 2):
-            out = torch.empty((2, 3, n), dtype=torch.float64, device=dev)
-            cnt = torch.empty(n, dtype=torch.uint8, device=dev)
-            st = torch.cuda.current_stream()
-            call = lambda: f(a.data_ptr(), b.data_ptr(), z0.data_ptr(), n, n, out.data_ptr(),
-                             cnt.data_ptr(), mode, ctypes.c_void_p(st.cuda_stream))
-            for _ in range(5):
-                assert call() == 0
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            reps = 50
-            e0.record()
-            for _ in range(reps):
-                call()
-            e1.record()
-            torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1) / reps
-            key = mode
-            if key not in ref:
-                ref[key] = (out.clone(), cnt.clone())
-            same = torch.equal(cnt, ref[key][1]) and torch.equal(
-                out.view(torch.int64), ref[key][0].view(torch.int64))
-            rows.append({"variant": name, "mode": mode, "ms": round(ms, 4),
-                         "Garcs_s": round(n / ms / 1e6, 2), "bitwise_same_as_base": same})
-            print(json.dumps(rows[-1]), flush=True)
+        fns[name] = f
+    modes = (1, 0)
+    times = {(v, m): [] for v in VARIANTS for m in modes}
+    clocks = []
+    ref = {}
+    same = {}
+    for r in range(rounds):
+        for name, f in fns.items():
+            for mode in modes:
+                call = lambda: f(a.data_ptr(), b.data_ptr(), z0.data_ptr(), n, n, out.data_ptr(),  # noqa: E731
+                                 cnt.data_ptr(), mode, ctypes.c_void_p(st.cuda_stream))
+                for _ in range(3):
+                    assert call() == 0
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(reps):
+                    call()
+                e1.record()
+                torch.cuda.synchronize()
+                clocks.append(clock())
+                times[(name, mode)].append(e0.elapsed_time(e1) / reps)
+                if r == 0:
+                    if mode not in ref:
+                        ref[mode] = (out.clone(), cnt.clone())
+                    same[(name, mode)] = torch.equal(cnt, ref[mode][1]) and torch.equal(
+                        out.view(torch.int64), ref[mode][0].view(torch.int64))
+    rows = []
+    for (name, mode), ts in times.items():
+        med = statistics.median(ts)
+        rows.append({"variant": name, "mode": mode, "ms_median": round(med, 4),
+                     "ms_min": round(min(ts), 4), "Garcs_s": round(n / med / 1e6, 2),
+                     "bitwise_same_as_base": same[(name, mode)]})
+        print(json.dumps(rows[-1]), flush=True)
+    print(json.dumps({"sm_clock_mhz_min": min(clocks), "sm_clock_mhz_median":
+                      statistics.median(clocks), "sm_clock_mhz_max": max(clocks)}))
     return rows
 
 
