@@ -128,17 +128,11 @@ def cpu_baseline_run(config: int, n: int, mode: str):
     return n / dt, cores, dt
 
 
-def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
-
-
 def run_reference(args):
     """--impl reference: the oracle on the host cores, each step a bounded sample (2^22 arcs)
     of the same workload; rank 0 only."""
-    ws, rank, _ = dist_env()
+    from paper_2510_09892_b200 import dist as sdist
+    ws, rank, _ = sdist.env()
     if rank != 0:
         return
     import oracle
@@ -178,16 +172,18 @@ def main():
     import torch.distributed as dist
     import paper_2510_09892_b200 as sgi
     import sgi_inputs
+    from paper_2510_09892_b200 import dist as sdist
 
-    ws, rank, local = dist_env()
+    ws, rank, local = sdist.env()
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if ws > 1:
+    distributed = "RANK" in os.environ                  # launched by torchrun (any world size)
+    if distributed:
         dist.init_process_group("nccl", device_id=dev)
     n, cfg, mode = args.n, args.config, args.mode
-    offset = rank * n                                   # this rank's slice of the index space
+    offset, n = sdist.shard_weak(rank, ws, n)           # this rank's slice of the index space
 
     # inputs generated on this rank's device from the seed (HBM resident before timing)
     a = torch.empty((3, n), dtype=torch.float64, device=dev)
@@ -204,7 +200,7 @@ def main():
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
-    if ws > 1:
+    if distributed:
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -214,14 +210,13 @@ def main():
             step()
         e1.record(stream)
         torch.cuda.synchronize()
-    if ws > 1:
+    if distributed:
         dist.barrier()
     ms_local = e0.elapsed_time(e1)
     t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
     hist = sgi.count_histogram(cnt)                    # outside the timed region
-    if ws > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(hist, op=dist.ReduceOp.SUM)
+    if distributed:                                    # MAX of time, SUM of counts (NCCL)
+        sdist.reduce_after_step(t, hist)
     ms = float(t.item())
     total_arcs = n * ws * args.steps
     value = total_arcs / (ms * 1e-3)
@@ -265,7 +260,7 @@ def main():
                                        work=work, stream=stream)
         e2e_step()
         torch.cuda.synchronize()
-        if ws > 1:
+        if distributed:
             dist.barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
@@ -274,7 +269,7 @@ def main():
         f1.record(stream)
         torch.cuda.synchronize()
         te = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
-        if ws > 1:
+        if distributed:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": n * ws * args.e2e_steps / (float(te.item()) * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": n * 56 * ws, "d2h_bytes_per_step": n * 49 * ws,
@@ -308,7 +303,7 @@ def main():
             "points_per_s": h[4] / (ms_per_step * 1e-3),
         }
         print(json.dumps(line), flush=True)
-    if ws > 1:
+    if distributed:
         dist.destroy_process_group()
 
 

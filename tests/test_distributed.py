@@ -1,0 +1,75 @@
+"""Multi-process (gloo, world size 2, CPU) test of the sharding and the post-step reduction used
+by bench.py's torchrun path: the shards' union is the global index range, and the reduced
+histogram equals the single-process one (the hot path is replaced by oracle (a) on CPU; the GPU
+kernel's R-invariance is tested separately in test_gpu_parity.py)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import sgi_inputs
+from paper_2510_09892_b200 import dist as sdist
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _hist(cnt):
+    return np.array([(cnt == 0).sum(), (cnt == 1).sum(), (cnt == 2).sum(), (cnt == 0xFF).sum(),
+                     (cnt == 1).sum() + 2 * (cnt == 2).sum()], np.int64)
+
+
+def _worker(rank, world, port, n_per_rank, config, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ws, r, _ = sdist.env()
+    off, cnt_n = sdist.shard_weak(r, ws, n_per_rank)
+    a, b, z0 = sgi_inputs.generate_host(config, cnt_n, offset=off)
+    _, cnt = oracle.intersect(oracle.MODE_EFT, a, b, z0)
+    hist = torch.from_numpy(_hist(cnt))
+    t = torch.tensor([10.0 + r], dtype=torch.float64)
+    t, hist = sdist.reduce_after_step(t, hist)
+    q.put((r, float(t.item()), hist.numpy().tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("config", [5, 3])
+def test_gloo_world2_sharded_histogram(config):
+    world, n = 2, 3000
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, config, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    a, b, z0 = sgi_inputs.generate_host(config, world * n)
+    _, cnt = oracle.intersect(oracle.MODE_EFT, a, b, z0)
+    want = _hist(cnt).tolist()
+    for r, t, h in res:
+        assert t == 11.0                       # MAX over ranks
+        assert h == want                       # SUM of shard histograms == global histogram
+
+
+def test_shard_ranges():
+    for world in (1, 2, 4, 8):
+        spans = [sdist.shard_strong(r, world, 1 << 30) for r in range(world)]
+        assert spans[0][0] == 0 and sum(c for _, c in spans) == 1 << 30
+        assert all(spans[i][0] + spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+        weak = [sdist.shard_weak(r, world, 1 << 24) for r in range(world)]
+        assert all(o == r << 24 and c == 1 << 24 for r, (o, c) in enumerate(weak))
+    with pytest.raises(ValueError):
+        sdist.shard_weak(2, 2, 10)
