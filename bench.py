@@ -113,6 +113,36 @@ class ClockSampler:
         return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(s)}
 
 
+def pcie_concurrent_gbs(dev, nbytes=1 << 29):
+    """Measured host<->device bandwidth with H2D and D2H running at once (pinned, CUDA events):
+    the ceiling of the e2e path, which moves 56 B in and 49 B out per query."""
+    import torch
+    n = nbytes // 8
+    hi = torch.empty(n, dtype=torch.float64).pin_memory()
+    ho = torch.empty(n, dtype=torch.float64).pin_memory()
+    di = torch.empty(n, dtype=torch.float64, device=dev)
+    do = torch.empty(n, dtype=torch.float64, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    cur = torch.cuda.current_stream(dev)
+    best = 0.0
+    for _ in range(3):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(cur)
+        s1.wait_stream(cur)
+        s2.wait_stream(cur)
+        with torch.cuda.stream(s1):
+            di.copy_(hi, non_blocking=True)
+        with torch.cuda.stream(s2):
+            ho.copy_(do, non_blocking=True)
+        cur.wait_stream(s1)
+        cur.wait_stream(s2)
+        e1.record(cur)
+        torch.cuda.synchronize()
+        best = max(best, 2 * nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+    return best
+
+
 def cpu_baseline_run(config: int, n: int, mode: str):
     """Oracle (a) as it stands (oracle/eft_oracle.c, OpenMP over all host cores) on the whole
     per-rank batch of the same workload; returns (arcs/s, cores, seconds)."""
@@ -271,9 +301,12 @@ def main():
         te = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
         if distributed:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": n * ws * args.e2e_steps / (float(te.item()) * 1e-3), "unit": UNIT,
+        e2e_s = float(te.item()) * 1e-3 / args.e2e_steps
+        link = pcie_concurrent_gbs(dev)
+        e2e = {"value": n * ws / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": n * 56 * ws, "d2h_bytes_per_step": n * 49 * ws,
-               "steps": args.e2e_steps, "path": "sgi_intersect_arc_lat_host (pinned host buffers)"}
+               "steps": args.e2e_steps, "path": "sgi_intersect_arc_lat_host (pinned host buffers)",
+               "link_gbs_measured": link, "link_frac": (n * 105 / e2e_s / 1e9) / link}
         del ha, hb, hz, hout, hcnt, work
 
     cpu = None

@@ -65,13 +65,14 @@ sgi_status sgi_intersect_arc_lat(const double* a, const double* b, const double*
  * pointers in the layout above (page-locked memory lets the copies overlap; pageable works).
  * d_work is a caller-owned device buffer of work_bytes >= sgi_host_workspace_bytes(chunk)
  * bytes for some chunk >= 1; the batch is streamed through it in chunks, copies and kernels
- * pipelined over `stream` and one internal stream.  Blocks until the results are on the host. */
+ * pipelined over `stream` and two internal streams (three buffers).  Blocks until the results
+ * are on the host. */
 sgi_status sgi_intersect_arc_lat_host(const double* a, const double* b, const double* z0,
                                       int64_t n, int64_t ld, double* out_xyz,
                                       uint8_t* out_count, int mode, void* d_work,
                                       size_t work_bytes, void* stream);
 
-/* Device bytes sgi_intersect_arc_lat_host needs for a given chunk length (two buffers). */
+/* Device bytes sgi_intersect_arc_lat_host needs for a given chunk length (three buffers). */
 size_t sgi_host_workspace_bytes(int64_t chunk);
 
 /* Histogram of out_count (device pointers): d_hist5[0..2] += number of queries with 0/1/2

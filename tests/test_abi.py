@@ -47,8 +47,8 @@ def test_version_and_status_strings(lib):
 
 def test_workspace_bytes(lib):
     assert sgi.host_workspace_bytes(0) == 0
-    assert sgi.host_workspace_bytes(1) == 2 * (13 * 256 + 256)
-    assert sgi.host_workspace_bytes(1 << 20) == 2 * (13 * (8 << 20) + (1 << 20))
+    assert sgi.host_workspace_bytes(1) == 3 * (13 * 256 + 256)
+    assert sgi.host_workspace_bytes(1 << 20) == 3 * (13 * (8 << 20) + (1 << 20))
 
 
 def _call(lib, a, b, z, n, ld, out, cnt, mode):

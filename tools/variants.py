@@ -17,19 +17,12 @@ OUT = os.path.join(ROOT, "build", "variants")
 
 VARIANTS = {
     "base": {},
-    "ldg": {'SGI_USE_TMA': 0},
-    "e256_s2": {'SGI_EFT_THREADS': 256, 'SGI_EFT_STAGES': 2, 'SGI_NAIVE_THREADS': 256, 'SGI_NAIVE_STAGES': 2},
-    "e256_s3": {'SGI_EFT_THREADS': 256, 'SGI_EFT_STAGES': 3, 'SGI_NAIVE_THREADS': 256, 'SGI_NAIVE_STAGES': 3},
-    "e384_s2": {'SGI_EFT_THREADS': 384, 'SGI_EFT_STAGES': 2, 'SGI_NAIVE_THREADS': 256, 'SGI_NAIVE_STAGES': 2},
-    "e384_s3": {'SGI_EFT_THREADS': 384, 'SGI_EFT_STAGES': 3, 'SGI_NAIVE_THREADS': 256, 'SGI_NAIVE_STAGES': 3},
-    "e512_s2": {'SGI_EFT_THREADS': 512, 'SGI_EFT_STAGES': 2, 'SGI_NAIVE_THREADS': 512, 'SGI_NAIVE_STAGES': 3},
-    "e512_s3": {'SGI_EFT_THREADS': 512, 'SGI_EFT_STAGES': 3, 'SGI_NAIVE_THREADS': 512, 'SGI_NAIVE_STAGES': 4},
-    "e640_s2": {'SGI_EFT_THREADS': 640, 'SGI_EFT_STAGES': 2, 'SGI_NAIVE_THREADS': 512, 'SGI_NAIVE_STAGES': 2},
-    "e640_s3": {'SGI_EFT_THREADS': 640, 'SGI_EFT_STAGES': 3, 'SGI_NAIVE_THREADS': 512, 'SGI_NAIVE_STAGES': 3},
-    "e768_s2": {'SGI_EFT_THREADS': 768, 'SGI_EFT_STAGES': 2, 'SGI_NAIVE_THREADS': 128, 'SGI_NAIVE_STAGES': 2},
-    "e768_s3": {'SGI_EFT_THREADS': 768, 'SGI_EFT_STAGES': 3, 'SGI_NAIVE_THREADS': 128, 'SGI_NAIVE_STAGES': 3},
-    "e1024_s2": {'SGI_EFT_THREADS': 1024, 'SGI_EFT_STAGES': 2, 'SGI_NAIVE_THREADS': 256, 'SGI_NAIVE_STAGES': 3},
-    "e1024_s3": {'SGI_EFT_THREADS': 1024, 'SGI_EFT_STAGES': 3, 'SGI_NAIVE_THREADS': 256, 'SGI_NAIVE_STAGES': 4},
+    "e512_s2": {'SGI_EFT_STAGES': 2},
+    "e512_s4": {'SGI_EFT_STAGES': 4},
+    "e512_s5": {'SGI_EFT_STAGES': 5},
+    "e512_s6": {'SGI_EFT_STAGES': 6},
+    "e256_s6": {'SGI_EFT_THREADS': 256, 'SGI_EFT_STAGES': 6},
+    "e384_s5": {'SGI_EFT_THREADS': 384, 'SGI_EFT_STAGES': 5},
 }
 
 
@@ -76,7 +69,7 @@ def time_all(n, rounds=7, reps=20):
         f.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int64] * 2 + [ctypes.c_void_p] * 2 + \
             [ctypes.c_int, ctypes.c_void_p]
         fns[name] = f
-    modes = (1, 0)
+    modes = (1,)
     times = {(v, m): [] for v in VARIANTS for m in modes}
     clocks = []
     ref = {}
