@@ -51,6 +51,9 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--workload", default="arcs", choices=["arcs", "zonal"],
+                   help="arcs: the C2/C3/C5 batch (default line); zonal: the fused zonal-mean "
+                        "pass over the C4 cubed sphere (ne=1024) x 1,800 latitudes")
     return p.parse_args()
 
 
@@ -193,10 +196,69 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+ZONAL_HEAD_OPS = 134    # per edge: AccuX lines 2-6 (114) + z-range filter (20), DESIGN.md §5
+ZONAL_TAIL_OPS = 248    # per candidate pair: AccuX lines 7-25 + containment
+
+
+def run_zonal(args):
+    """Fused zonal-mean pass (sgi_zonal_intersect) over the C4 mesh; one step = one launch over
+    all 12.6 M edges; value = candidate (edge, latitude) pairs per second (single GPU)."""
+    import torch
+    import paper_2510_09892_b200 as sgi
+    import sgi_inputs
+    dev = torch.device("cuda", 0)
+    va, vb = sgi_inputs.cubed_sphere_edges(1024)
+    lat = sgi_inputs.latitudes(1800)
+    dva, dvb = torch.from_numpy(va).to(dev), torch.from_numpy(vb).to(dev)
+    dl = torch.from_numpy(lat).to(dev)
+    ne = va.shape[1]
+    first = sgi.zonal_intersect(dva, dvb, dl, mode=args.mode)
+    torch.cuda.synchronize()
+    cap = first["cap"]
+    work = torch.empty(sgi.zonal_workspace_bytes(ne), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        sgi.zonal_intersect(dva, dvb, dl, mode=args.mode, cap=cap, stream=stream, work=work)
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clocks:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    s = e0.elapsed_time(e1) * 1e-3 / args.steps
+    cnt = first["count"][:cap].cpu()
+    nz = int((cnt != 0).sum())
+    peaks = load_peaks()
+    alu_peak = 148 * 64 * peaks["sm_max_mhz"] * 1e6 / 1e12
+    ops = ne * ZONAL_HEAD_OPS + cap * ZONAL_TAIL_OPS
+    byts = ne * 48 + cap * (8 + 4 + 1 + 48)
+    line = {"metric": "zonal (edge, latitude) candidate pairs/s", "value": cap / s,
+            "unit": "pairs/s", "n_gpus": 1, "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": s * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C4 cubed sphere ne=1024 (12,582,912 edges) x 1,800 latitudes, "
+                                   "fused sgi_zonal_intersect", "mode": args.mode,
+                       "pairs": cap, "nonzero_pairs": nz, "edges_per_s": ne / s},
+            "roofline": {"bound": "alu" if ops / (alu_peak * 1e12) > byts / (peaks["hbm_gbs"] * 1e9)
+                         else "hbm",
+                         "alu_frac": ops / s / 1e12 / alu_peak,
+                         "hbm_frac": byts / s / 1e9 / peaks["hbm_gbs"],
+                         "peak_alu": alu_peak, "peak_hbm": peaks["hbm_gbs"]},
+            "clocks": clocks.summary(), "gpu_launches": args.steps}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "zonal":
+        return run_zonal(args)
 
     import torch
     import torch.distributed as dist

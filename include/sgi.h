@@ -81,6 +81,28 @@ size_t sgi_host_workspace_bytes(int64_t chunk);
 sgi_status sgi_count_histogram(const uint8_t* out_count, int64_t n,
                                unsigned long long* d_hist5, void* stream);
 
+/* Fused zonal-mean pass (zonal means on regridding meshes): every mesh
+ * edge (va_e, vb_e) against a latitude table, compacted.  Edges are SoA planes va[c*ld_e + e],
+ * vb[c*ld_e + e] (device); lat_z0[n_lat] is strictly increasing (device).  For each edge, the
+ * candidate latitudes are those within delta = 2^-40 of the arc's z-range (endpoint heights
+ * z/|x| and, when the great circle's extremum lies inside the arc, the apex height
+ * sqrt(|n_xy|^2/|n|^2), from the EFT normal); an edge with n = 0 (degenerate at every
+ * latitude) has every latitude as a candidate.  Every (edge, latitude) whose query has a
+ * nonzero count is a candidate; candidates within delta of the range may have count 0.
+ * Candidate pair j (edge-major, latitude ascending; deterministic) is written to out_edge[j],
+ * out_lat[j], out_count[j] and out_xyz[(slot*3 + c)*cap + j], bit-identical to
+ * sgi_intersect_arc_lat on (va_e, vb_e, lat_z0[k]) in `mode`.  Pairs j >= cap are not written;
+ * *d_total (device) receives the number of candidate pairs, so cap = 0 is a count-only call.
+ * d_work: caller-owned device workspace of sgi_zonal_workspace_bytes(n_edges) bytes.  n_lat
+ * <= 2^23.  Asynchronous on `stream` (three launches: count, scan, emit).  Errors as for
+ * sgi_intersect_arc_lat. */
+sgi_status sgi_zonal_intersect(const double* va, const double* vb, int64_t n_edges,
+                               int64_t ld_e, const double* lat_z0, int32_t n_lat, int64_t cap,
+                               int64_t* out_edge, int32_t* out_lat, uint8_t* out_count,
+                               double* out_xyz, unsigned long long* d_total, void* d_work,
+                               size_t work_bytes, int mode, void* stream);
+size_t sgi_zonal_workspace_bytes(int64_t n_edges);
+
 const char* sgi_status_str(sgi_status s);
 const char* sgi_last_error(void);
 int sgi_abi_version(void);

@@ -8,6 +8,7 @@ Public API (same names as the C ABI):
     intersect_arc_lat(a, b, z0, mode="eft", out_xyz=None, out_count=None, n=None, stream=None)
     intersect_arc_lat_host(a, b, z0, mode="eft", out_xyz=None, out_count=None, work=None, ...)
     count_histogram(out_count, n=None, hist=None, stream=None)
+    zonal_intersect(va, vb, lat_z0, mode="eft", cap=None, stream=None)
     host_workspace_bytes(chunk), abi_version(), status_str(code), last_error()
 Layout: a[3, ld], b[3, ld], z0[ld] float64; out_xyz[2, 3, ld] float64; out_count[ld] uint8.
 """
@@ -46,6 +47,11 @@ def _load():
         L.sgi_host_workspace_bytes.argtypes = [i64]
         L.sgi_count_histogram.restype = ctypes.c_int
         L.sgi_count_histogram.argtypes = [vp, i64, vp, vp]
+        L.sgi_zonal_intersect.restype = ctypes.c_int
+        L.sgi_zonal_intersect.argtypes = [vp, vp, i64, i64, vp, ctypes.c_int32, i64, vp, vp, vp,
+                                          vp, vp, vp, ctypes.c_size_t, ctypes.c_int, vp]
+        L.sgi_zonal_workspace_bytes.restype = ctypes.c_size_t
+        L.sgi_zonal_workspace_bytes.argtypes = [i64]
         L.sgi_status_str.restype = ctypes.c_char_p
         L.sgi_status_str.argtypes = [ctypes.c_int]
         L.sgi_last_error.restype = ctypes.c_char_p
@@ -161,3 +167,47 @@ def count_histogram(out_count, n=None, hist=None, stream=None):
     rc = _load().sgi_count_histogram(out_count.data_ptr(), n, hist.data_ptr(), _stream_ptr(stream))
     _check(rc, "sgi_count_histogram")
     return hist
+
+
+def zonal_workspace_bytes(n_edges: int) -> int:
+    return int(_load().sgi_zonal_workspace_bytes(n_edges))
+
+
+def zonal_intersect(va, vb, lat_z0, mode="eft", cap=None, n_edges=None, stream=None, work=None):
+    """Fused zonal-mean pass (sgi_zonal_intersect): CUDA float64 edges va[3, ld], vb[3, ld] and a
+    strictly increasing latitude table lat_z0[K] -> dict(edge int64, lat int32, count uint8,
+    xyz float64 [2, 3, m]) over the m candidate pairs, edge-major, latitude ascending.
+
+    With cap=None a count-only call sizes the outputs first (one synchronisation)."""
+    import torch
+    ld = va.shape[1]
+    n_edges = ld if n_edges is None else n_edges
+    _cuda_f64(va, (3, ld), "va")
+    _cuda_f64(vb, (3, ld), "vb")
+    _cuda_f64(lat_z0, (lat_z0.shape[0],), "lat_z0")
+    dev = va.device
+    L = _load()
+    if work is None:
+        work = torch.empty(max(zonal_workspace_bytes(n_edges), 8), dtype=torch.uint8, device=dev)
+    total = torch.zeros(1, dtype=torch.int64, device=dev)
+    sp = _stream_ptr(stream)
+    if cap is None:
+        rc = L.sgi_zonal_intersect(va.data_ptr(), vb.data_ptr(), n_edges, ld, lat_z0.data_ptr(),
+                                   lat_z0.shape[0], 0, None, None, None, None, total.data_ptr(),
+                                   work.data_ptr(), work.numel(), _mode(mode), sp)
+        _check(rc, "sgi_zonal_intersect (count)")
+        (torch.cuda.current_stream() if stream is None else stream).synchronize()
+        cap = int(total.item())
+    cap_alloc = max(cap, 1)
+    out = {"edge": torch.empty(cap_alloc, dtype=torch.int64, device=dev),
+           "lat": torch.empty(cap_alloc, dtype=torch.int32, device=dev),
+           "count": torch.empty(cap_alloc, dtype=torch.uint8, device=dev),
+           "xyz": torch.empty((2, 3, cap_alloc), dtype=torch.float64, device=dev)}
+    rc = L.sgi_zonal_intersect(va.data_ptr(), vb.data_ptr(), n_edges, ld, lat_z0.data_ptr(),
+                               lat_z0.shape[0], cap, out["edge"].data_ptr(), out["lat"].data_ptr(),
+                               out["count"].data_ptr(), out["xyz"].data_ptr(), total.data_ptr(),
+                               work.data_ptr(), work.numel(), _mode(mode), sp)
+    _check(rc, "sgi_zonal_intersect")
+    out["total"] = total
+    out["cap"] = cap
+    return out

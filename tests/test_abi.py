@@ -27,7 +27,8 @@ def declared_symbols():
 def test_header_declares_the_boundary():
     assert declared_symbols() == sorted([
         "sgi_intersect_arc_lat", "sgi_intersect_arc_lat_host", "sgi_host_workspace_bytes",
-        "sgi_count_histogram", "sgi_status_str", "sgi_last_error", "sgi_abi_version"])
+        "sgi_count_histogram", "sgi_status_str", "sgi_last_error", "sgi_abi_version",
+        "sgi_zonal_intersect", "sgi_zonal_workspace_bytes"])
 
 
 def test_library_exports_every_declared_symbol(lib):
@@ -74,6 +75,17 @@ def test_invalid_arguments_rejected_without_launch(lib):
     assert _call(lib, None, None, None, 0, 0, None, None, 1) == sgi.SGI_OK
     assert lib.sgi_count_histogram(None, -1, None, None) == sgi.SGI_E_INVALID
     assert lib.sgi_count_histogram(None, 0, None, None) == sgi.SGI_OK
+
+
+def test_zonal_validates_arguments(lib):
+    tot = np.zeros(1, np.uint64)
+    assert lib.sgi_zonal_intersect(None, None, -1, 0, None, 0, 0, None, None, None, None,
+                                   tot.ctypes.data, None, 0, 1, None) == sgi.SGI_E_INVALID
+    e = np.zeros((3, 8)); lat = np.zeros(4)
+    assert lib.sgi_zonal_intersect(e.ctypes.data, e.ctypes.data, 8, 8, lat.ctypes.data, 4, 0,
+                                   None, None, None, None, tot.ctypes.data, None, 0, 1,
+                                   None) == sgi.SGI_E_INVALID          # no workspace
+    assert sgi.zonal_workspace_bytes(0) == 32768 and sgi.zonal_workspace_bytes(1 << 30) == 32768
 
 
 def test_host_entry_validates_workspace(lib):

@@ -1,0 +1,150 @@
+"""GPU tests of the fused zonal-mean pass (sgi_zonal_intersect).
+
+  * the candidate filter is conservative: every (edge, latitude) with a nonzero count under
+    brute force (oracle (a) on ALL pairs) is a candidate;
+  * every candidate's count and points equal oracle (a) on that pair (parity up to the sign of
+    zero) — i.e. the fused head/tail split is the plain query;
+  * candidates with count 0 sit within 2 * 2^-40 of the arc's z-range (oracle (b), shifted z0);
+  * output order is edge-major, latitude ascending; the run is bitwise repeatable; cap
+    truncation and count-only calls report the same total; large tables use the global path;
+  * the full C4 workload (cubed sphere ne=1024 x 1,800 latitudes) gives the same nonzero pairs
+    and values as the unfused kernel on the materialised pairs.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import sgi_inputs
+from oracle import exact
+
+torch = pytest.importorskip("torch")
+import paper_2510_09892_b200 as sgi  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DELTA = 2.0 ** -40
+
+
+def same(x, y):
+    return (x == y) | (np.isnan(x) & np.isnan(y))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _build():
+    sgi.build()
+
+
+def run_zonal(va, vb, lat, mode="eft", cap=None):
+    dva = torch.from_numpy(np.ascontiguousarray(va)).cuda()
+    dvb = torch.from_numpy(np.ascontiguousarray(vb)).cuda()
+    dl = torch.from_numpy(np.ascontiguousarray(lat)).cuda()
+    out = sgi.zonal_intersect(dva, dvb, dl, mode=mode, cap=cap)
+    torch.cuda.synchronize()
+    m = min(out["cap"], int(out["total"].item()))
+    return ({k: v[..., :m].cpu().numpy() for k, v in out.items() if k in ("edge", "lat", "count", "xyz")},
+            int(out["total"].item()))
+
+
+def brute_force(va, vb, lat, mode):
+    """oracle (a) on every (edge, latitude) pair; returns counts [E, K] and points."""
+    E, K = va.shape[1], len(lat)
+    a = np.repeat(va, K, axis=1)
+    b = np.repeat(vb, K, axis=1)
+    z = np.tile(lat, E)
+    out, cnt = oracle.intersect(mode, a, b, z, nthreads=16)
+    return cnt.reshape(E, K), out.reshape(2, 3, E, K)
+
+
+def check_against_brute(va, vb, lat, mode_name, omode):
+    res, total = run_zonal(va, vb, lat, mode_name)
+    cnt, pts = brute_force(va, vb, lat, omode)
+    e, k = res["edge"], res["lat"]
+    assert total == len(e)
+    # order: edge-major, latitude ascending
+    key = e.astype(np.int64) * len(lat) + k
+    assert np.all(np.diff(key) > 0)
+    # conservative: all nonzero pairs are candidates
+    nz = np.argwhere(cnt != 0)
+    cand = set(key.tolist())
+    missing = [tuple(p) for p in nz if p[0] * len(lat) + p[1] not in cand]
+    assert missing == [], missing[:5]
+    # values equal the plain query
+    assert np.array_equal(res["count"], cnt[e, k])
+    assert same(res["xyz"], pts[:, :, e, k]).all()
+    return res, cnt
+
+
+def test_small_mesh_against_brute_force():
+    va, vb = sgi_inputs.cubed_sphere_edges(16)
+    lat = sgi_inputs.latitudes(1800)
+    res, cnt = check_against_brute(va, vb, lat, "eft", oracle.MODE_EFT)
+    zero = np.flatnonzero(res["count"] == 0)
+    for j in zero[:200]:                      # margin candidates lie within 2*delta of the arc
+        e, k = res["edge"][j], res["lat"][j]
+        hits = [exact.exact_query(va[:, e], vb[:, e], lat[k] + s * 2 * DELTA).count
+                for s in (-1.0, 1.0)]
+        assert any(h not in (0,) for h in hits)
+
+
+@pytest.mark.parametrize("mode,omode", [("eft", oracle.MODE_EFT), ("eft_literal", oracle.MODE_EFT_LITERAL),
+                                        ("naive", oracle.MODE_NAIVE)])
+def test_long_arcs_many_latitudes(mode, omode):
+    """C1 arcs (long, up to pi) against 181 latitudes: edges spanning many latitudes, two-point
+    pairs, dense redistribution of candidates across threads."""
+    a, b, _ = sgi_inputs.generate_host(1, 700)
+    lat = np.sin(np.radians(np.linspace(-90, 90, 183)[1:-1]))
+    res, cnt = check_against_brute(a, b, lat, mode, omode)
+    assert (res["count"] == 2).sum() > 0 and (np.bincount(res["edge"]) > 20).any()
+
+
+def test_degenerate_and_special_edges():
+    va = np.array([[1, 0, 0], [1, 0, 0], [0.6, 0, 0.8], [1, 0, 1], [1, 0, -1], [0, 0, 1]], float).T.copy()
+    vb = np.array([[0, 1, 0], [0, 0, 1], [0.6, 0, 0.8], [-1, 0, 1], [-1, 0, -1], [1, 0, 0]], float).T.copy()
+    lat = np.array([-0.75, -0.5, 0.0, 0.5, 0.75, 0.8, 1.0])
+    check_against_brute(va, vb, lat, "eft", oracle.MODE_EFT)
+
+
+def test_repeatable_truncation_and_count_only():
+    a, b, _ = sgi_inputs.generate_host(5, 20000)
+    lat = sgi_inputs.latitudes(1800)
+    r1, t1 = run_zonal(a, b, lat)
+    r2, t2 = run_zonal(a, b, lat)
+    assert t1 == t2 and all(np.array_equal(r1[k].view(np.uint8), r2[k].view(np.uint8)) for k in r1)
+    r3, t3 = run_zonal(a, b, lat, cap=t1 // 3)
+    assert t3 == t1 and len(r3["edge"]) == t1 // 3
+    assert np.array_equal(r3["edge"], r1["edge"][:t1 // 3]) and same(r3["xyz"], r1["xyz"][:, :, :t1 // 3]).all()
+
+
+def test_large_latitude_table_global_path():
+    a, b, _ = sgi_inputs.generate_host(2, 1000)
+    lat = np.sin(np.radians(-90 + (np.arange(10000) + 0.5) * 180 / 10000))
+    check_against_brute(a, b, lat, "eft", oracle.MODE_EFT)
+
+
+def test_empty_inputs():
+    va = np.zeros((3, 0)); lat = sgi_inputs.latitudes(10)
+    res, total = run_zonal(va, va, lat)
+    assert total == 0
+    a, b, _ = sgi_inputs.generate_host(1, 100)
+    res, total = run_zonal(a, b, np.zeros(0))
+    assert total == 0
+
+
+def test_c4_full_size_against_unfused_path():
+    va, vb = sgi_inputs.cubed_sphere_edges(1024)
+    lat = sgi_inputs.latitudes(1800)
+    res, total = run_zonal(va, vb, lat)
+    pa, pb, pz, pe = sgi_inputs.c4_pairs(1024, 1800)
+    da, db, dz = (torch.from_numpy(x).cuda() for x in (pa, pb, pz))
+    out, cnt = sgi.intersect_arc_lat(da, db, dz, mode="eft")
+    torch.cuda.synchronize()
+    out, cnt = out.cpu().numpy(), cnt.cpu().numpy()
+    k_of = np.searchsorted(lat, pz)
+    nz_unfused = set((pe[cnt != 0] * 1800 + k_of[cnt != 0]).tolist())
+    key = res["edge"] * 1800 + res["lat"]
+    nzmask = res["count"] != 0
+    assert set(key[nzmask].tolist()) == nz_unfused
+    # values: fused pairs that the numpy pairing also produced must be bit-equal
+    _, jf, ju = np.intersect1d(key, pe * 1800 + k_of, assume_unique=True, return_indices=True)
+    assert np.array_equal(res["count"][jf], cnt[ju])
+    assert same(res["xyz"][:, :, jf], out[:, :, ju]).all()
+    assert total >= len(nz_unfused) and len(nz_unfused) > 5_900_000
