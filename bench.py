@@ -31,7 +31,7 @@ UNIT = "intersections/s"
 BYTES_PER_ARC = 56 + 48 + 1          # a, b, z0 in; two xyz slots + uint8 count out (§8(b))
 # Algorithmic FP64 operations per query (add/sub/mul/fma/div/sqrt = 1 each) of the op sequence
 # in csrc/sgi_query.cuh; derivation in DESIGN.md §5.
-FP64_OPS = {"eft": 362, "eft_literal": 347, "naive": 42}
+FP64_OPS = {"eft": 362, "eft_literal": 347, "naive": 42, "yac": 48, "base": 47, "naive_kahan": 45}
 SEEDS = {2: 2, 3: 3, 5: 5}
 CONFIG_DESC = {
     2: "C2 short arcs (midpoint uniform, length log-uniform [1e-4,1e-2] rad, z0 between endpoint z)",
@@ -45,7 +45,8 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=10)
-    p.add_argument("--mode", default="eft", choices=["eft", "eft_literal", "naive"])
+    p.add_argument("--mode", default="eft",
+                   choices=["eft", "eft_literal", "naive", "yac", "base", "naive_kahan"])
     p.add_argument("--config", type=int, default=2, choices=[2, 3, 5])
     p.add_argument("--n", type=int, default=1 << 24, help="arcs per rank")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -153,7 +154,8 @@ def cpu_baseline_run(config: int, n: int, mode: str):
     import sgi_inputs
     cores = os.cpu_count() or 1
     a, b, z0 = sgi_inputs.generate_host(config, n, seed=SEEDS[config])
-    m = {"eft": oracle.MODE_EFT, "eft_literal": oracle.MODE_EFT_LITERAL, "naive": oracle.MODE_NAIVE}[mode]
+    m = {"eft": oracle.MODE_EFT, "eft_literal": oracle.MODE_EFT_LITERAL, "naive": oracle.MODE_NAIVE,
+         "yac": oracle.MODE_YAC, "base": oracle.MODE_BASE, "naive_kahan": oracle.MODE_NAIVE_KAHAN}[mode]
     oracle.intersect(m, a[:, :4096], b[:, :4096], z0[:4096], nthreads=cores)   # warm
     t0 = time.perf_counter()
     oracle.intersect(m, a, b, z0, nthreads=cores)
@@ -173,7 +175,9 @@ def run_reference(args):
     cores = os.cpu_count() or 1
     n = min(args.n, 1 << 22)
     a, b, z0 = sgi_inputs.generate_host(args.config, n, seed=SEEDS[args.config])
-    m = {"eft": oracle.MODE_EFT, "eft_literal": oracle.MODE_EFT_LITERAL, "naive": oracle.MODE_NAIVE}[args.mode]
+    m = {"eft": oracle.MODE_EFT, "eft_literal": oracle.MODE_EFT_LITERAL, "naive": oracle.MODE_NAIVE,
+         "yac": oracle.MODE_YAC, "base": oracle.MODE_BASE,
+         "naive_kahan": oracle.MODE_NAIVE_KAHAN}[args.mode]
     for _ in range(max(args.warmup, 0)):
         oracle.intersect(m, a, b, z0, nthreads=cores)
     steps = max(1, min(args.steps, 20))

@@ -16,6 +16,10 @@
  *                         Error bound 3 sqrt(1 - z0^2) u, u = 2^-53 (Eq.BOUND).
  *   SGI_MODE_EFT_LITERAL  AccuX exactly as listed (no renormalisation).
  *   SGI_MODE_NAIVE        Eq.FINAL in plain binary64 (§4).
+ *   SGI_MODE_YAC          Eq.YAC in plain binary64: normalised normal n/|n|.
+ *   SGI_MODE_BASE         Eq.BASE in plain binary64: divisor 1 - n^z^2.
+ *   SGI_MODE_NAIVE_KAHAN  Eq.FINAL in binary64 with Kahan's DiffOfProd normal (Alg.3).
+ * (the last three are the paper's comparison formulas)
  * Results are bit-identical to the CPU oracle's op sequence (oracle/eft_oracle.c) up to the sign
  * of zero, independent of grid shape, stream or sharding.
  *
@@ -51,7 +55,14 @@ extern "C" {
 #define SGI_ABI_VERSION 1
 #define SGI_DEGENERATE ((uint8_t)0xFF)
 
-typedef enum { SGI_MODE_NAIVE = 0, SGI_MODE_EFT = 1, SGI_MODE_EFT_LITERAL = 2 } sgi_mode;
+typedef enum {
+  SGI_MODE_NAIVE = 0,
+  SGI_MODE_EFT = 1,
+  SGI_MODE_EFT_LITERAL = 2,
+  SGI_MODE_YAC = 3,
+  SGI_MODE_BASE = 4,
+  SGI_MODE_NAIVE_KAHAN = 5
+} sgi_mode;
 typedef enum { SGI_OK = 0, SGI_E_INVALID = 1, SGI_E_CUDA = 2 } sgi_status;
 
 /* Device entry point.  a, b, z0, out_xyz, out_count are CUDA device pointers.  Enqueues one

@@ -22,6 +22,7 @@ LIB = os.path.join(_HERE, "liboracle_eft.so")
 SRC = os.path.join(_HERE, "eft_oracle.c")
 
 MODE_NAIVE, MODE_EFT, MODE_EFT_LITERAL = 0, 1, 2
+MODE_YAC, MODE_BASE, MODE_NAIVE_KAHAN = 3, 4, 5
 DEGENERATE = 0xFF
 
 TRACE_FIELDS = ("nx", "ex", "ny", "ey", "nz", "ez", "S2", "s2", "S3", "s3", "C", "eC", "D", "eD",

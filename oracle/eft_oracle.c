@@ -27,6 +27,8 @@
  *       P+ (ascending crossing) comes first iff g1 >= 0.
  *   R8  Naive mode ("pure floating-point implementation"; analysed in S1): plain cross
  *       product, no FMA, left-to-right products, 4 divisions.
+ *   R9  Comparison formulas Eq.YAC / Eq.BASE / Kahan-normal naive: the same plain, left-to-right
+ *       translation, normalising n with one sqrt and three divisions.
  *   parity unpinned: SGI_MODE_EFT_LITERAL on near-coincident endpoints (separation < 1e-7 rad)
  *   is outside the paper's nondegeneracy assumption; only bit-equality with the
  *   CUDA path is checked there, not the error bound.
@@ -136,7 +138,8 @@ static pair acc_sqrt(double H, double h) {
 
 /* ------------------------------------------------------------------------------------------- */
 /* Modes, identical numbering to include/sgi.h (declared independently here). */
-enum { OR_MODE_NAIVE = 0, OR_MODE_EFT = 1, OR_MODE_EFT_LITERAL = 2 };
+enum { OR_MODE_NAIVE = 0, OR_MODE_EFT = 1, OR_MODE_EFT_LITERAL = 2, OR_MODE_YAC = 3,
+       OR_MODE_BASE = 4, OR_MODE_NAIVE_KAHAN = 5 };
 #define OR_DEGENERATE 0xFF
 
 /* Trace of every AccuX intermediate, for the Appendix-A style pins. */
@@ -220,6 +223,48 @@ static void naive(const double x1[3], const double x2[3], double z0, accux_trace
   t->Pm[0] = -(Xm / S2); t->Pm[1] = -(Ym / S2);
 }
 
+/* The paper's comparison formulas in plain binary64 (reading R9):
+ *   YAC  Eq.YAC: hat n = n/|n|, s^ = sqrt(hx^2 + hy^2 - z0^2), divisor hx^2 + hy^2;
+ *   BASE Eq.BASE: divisor 1 - hz^2, s* = sqrt(1 - hz^2 - z0^2);
+ *   NAIVE_KAHAN  Eq.FINAL with each normal component by Kahan's DiffOfProd (Alg.3).
+ * hx, hy, hz return the normal the containment test uses (hat n; n itself for NAIVE_KAHAN). */
+static void variant(int mode, const double x1[3], const double x2[3], double z0, accux_trace* t,
+                    double* hx, double* hy, double* hz) {
+  double nx, ny, nz;
+  if (mode == OR_MODE_NAIVE_KAHAN) {
+    nx = kahan_dop(x1[1], x1[2], x2[1], x2[2]);   /* y1*z2 - z1*y2 */
+    ny = kahan_dop(x1[2], x1[0], x2[2], x2[0]);   /* z1*x2 - x1*z2 */
+    nz = kahan_dop(x1[0], x1[1], x2[0], x2[1]);   /* x1*y2 - y1*x2 */
+  } else {
+    nx = (x1[1] * x2[2]) - (x1[2] * x2[1]);
+    ny = (x1[2] * x2[0]) - (x1[0] * x2[2]);
+    nz = (x1[0] * x2[1]) - (x1[1] * x2[0]);
+  }
+  double S2 = (nx * nx) + (ny * ny);
+  double S3 = S2 + (nz * nz);
+  memset(t, 0, sizeof(*t));
+  t->nx = nx; t->ny = ny; t->nz = nz; t->S2 = S2; t->S3 = S3;
+  double ux = nx, uy = ny, uz = nz, den = S2, sh;
+  if (mode != OR_MODE_NAIVE_KAHAN) {
+    double N = sqrt(S3 > 0.0 ? S3 : 1.0);
+    ux = nx / N; uy = ny / N; uz = nz / N;
+    den = mode == OR_MODE_YAC ? (ux * ux) + (uy * uy) : 1.0 - (uz * uz);
+    sh = den - (z0 * z0);
+  } else {
+    sh = S2 - (S3 * (z0 * z0));
+  }
+  double s = sh > 0.0 ? sqrt(sh) : 0.0;
+  double bx = (z0 * ux) * uz, by = (z0 * uy) * uz;
+  double Xp = bx + (s * uy), Xm = bx - (s * uy);
+  double Yp = by - (s * ux), Ym = by + (s * ux);
+  t->sh = sh; t->s = s; t->Xp = Xp; t->Yp = Yp; t->Xm = Xm; t->Ym = Ym;
+  t->Pp[0] = -(Xp / den); t->Pp[1] = -(Yp / den);
+  t->Pm[0] = -(Xm / den); t->Pm[1] = -(Ym / den);
+  *hx = nx == 0.0 ? 0.0 : ux;
+  *hy = ny == 0.0 ? 0.0 : uy;
+  *hz = nz == 0.0 ? 0.0 : uz;
+}
+
 static double canonical_nan(void) {
   union { uint64_t u; double d; } c;
   c.u = 0x7FF8000000000000ull;
@@ -234,6 +279,8 @@ static uint8_t intersect_one(int mode, const double x1[3], const double x2[3], d
   if (mode == OR_MODE_NAIVE) {
     naive(x1, x2, z0, &t);
     hx = t.nx; hy = t.ny; hz = t.nz;
+  } else if (mode >= OR_MODE_YAC) {
+    variant(mode, x1, x2, z0, &t, &hx, &hy, &hz);
   } else {
     accux(x1, x2, z0, mode == OR_MODE_EFT, &t);
     if (mode == OR_MODE_EFT) { hx = t.nx; hy = t.ny; hz = t.nz; }
@@ -275,7 +322,7 @@ static uint8_t intersect_one(int mode, const double x1[3], const double x2[3], d
 int oracle_intersect_batch(int mode, const double* a, const double* b, const double* z0,
                            int64_t n, int64_t ld, double* out_xyz, uint8_t* out_count,
                            int nthreads) {
-  if (mode < 0 || mode > 2 || n < 0 || ld < n) return 1;
+  if (mode < 0 || mode > 5 || n < 0 || ld < n) return 1;
   if (nthreads < 1) nthreads = 1;
 #pragma omp parallel for schedule(static) num_threads(nthreads)
   for (int64_t i = 0; i < n; ++i) {

@@ -19,7 +19,7 @@ import os
 
 from ._build import LIB_PATH, build  # noqa: F401
 
-MODES = {"naive": 0, "eft": 1, "eft_literal": 2}
+MODES = {"naive": 0, "eft": 1, "eft_literal": 2, "yac": 3, "base": 4, "naive_kahan": 5}
 DEGENERATE = 0xFF
 SGI_OK, SGI_E_INVALID, SGI_E_CUDA = 0, 1, 2
 

@@ -292,7 +292,7 @@ sgi_status sgi_zonal_intersect(const double* va, const double* vb, int64_t n_edg
                                size_t work_bytes, int mode, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (n_edges < 0 || ld_e < n_edges || n_lat < 0 || n_lat > (1 << 23) || cap < 0 || mode < SGI_MODE_NAIVE ||
-      mode > SGI_MODE_EFT_LITERAL || !d_total) {
+      mode > SGI_MODE_NAIVE_KAHAN || !d_total) {
     sgi_internal::set_error_msg("sgi_zonal_intersect: invalid arguments", cudaSuccess);
     return SGI_E_INVALID;
   }
@@ -334,25 +334,26 @@ sgi_status sgi_zonal_intersect(const double* va, const double* vb, int64_t n_edg
   switch (mode) {
     case SGI_MODE_NAIVE: grid = grid_for(sgi_zonal_emit_kernel<sgi::MODE_NAIVE>, emit_smem); break;
     case SGI_MODE_EFT: grid = grid_for(sgi_zonal_emit_kernel<sgi::MODE_EFT>, emit_smem); break;
-    default: grid = grid_for(sgi_zonal_emit_kernel<sgi::MODE_EFT_LITERAL>, emit_smem); break;
+    case SGI_MODE_EFT_LITERAL: grid = grid_for(sgi_zonal_emit_kernel<sgi::MODE_EFT_LITERAL>, emit_smem); break;
+    case SGI_MODE_YAC: grid = grid_for(sgi_zonal_emit_kernel<sgi::MODE_YAC>, emit_smem); break;
+    case SGI_MODE_BASE: grid = grid_for(sgi_zonal_emit_kernel<sgi::MODE_BASE>, emit_smem); break;
+    default: grid = grid_for(sgi_zonal_emit_kernel<sgi::MODE_NAIVE_KAHAN>, emit_smem); break;
   }
   grid_for(sgi_zonal_count_kernel, lat_smem);
   sgi_zonal_count_kernel<<<grid, kTile, lat_smem, st>>>(va, vb, n_edges, ld_e, lat_z0, n_lat, cta);
   sgi_zonal_scan_kernel<<<1, 1024, 0, st>>>(cta, grid, d_total);
   if (cap > 0) {
+    auto emit = [&](auto kernel) {
+      kernel<<<grid, kTile, emit_smem, st>>>(va, vb, n_edges, ld_e, lat_z0, n_lat, cap, out_edge,
+                                             out_lat, out_count, out_xyz, cta);
+    };
     switch (mode) {
-      case SGI_MODE_NAIVE:
-        sgi_zonal_emit_kernel<sgi::MODE_NAIVE><<<grid, kTile, emit_smem, st>>>(
-            va, vb, n_edges, ld_e, lat_z0, n_lat, cap, out_edge, out_lat, out_count, out_xyz, cta);
-        break;
-      case SGI_MODE_EFT:
-        sgi_zonal_emit_kernel<sgi::MODE_EFT><<<grid, kTile, emit_smem, st>>>(
-            va, vb, n_edges, ld_e, lat_z0, n_lat, cap, out_edge, out_lat, out_count, out_xyz, cta);
-        break;
-      default:
-        sgi_zonal_emit_kernel<sgi::MODE_EFT_LITERAL><<<grid, kTile, emit_smem, st>>>(
-            va, vb, n_edges, ld_e, lat_z0, n_lat, cap, out_edge, out_lat, out_count, out_xyz, cta);
-        break;
+      case SGI_MODE_NAIVE: emit(sgi_zonal_emit_kernel<sgi::MODE_NAIVE>); break;
+      case SGI_MODE_EFT: emit(sgi_zonal_emit_kernel<sgi::MODE_EFT>); break;
+      case SGI_MODE_EFT_LITERAL: emit(sgi_zonal_emit_kernel<sgi::MODE_EFT_LITERAL>); break;
+      case SGI_MODE_YAC: emit(sgi_zonal_emit_kernel<sgi::MODE_YAC>); break;
+      case SGI_MODE_BASE: emit(sgi_zonal_emit_kernel<sgi::MODE_BASE>); break;
+      default: emit(sgi_zonal_emit_kernel<sgi::MODE_NAIVE_KAHAN>); break;
     }
   }
   e = cudaGetLastError();

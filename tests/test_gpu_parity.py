@@ -20,7 +20,8 @@ import paper_2510_09892_b200 as sgi  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 MODES = [("eft", oracle.MODE_EFT), ("eft_literal", oracle.MODE_EFT_LITERAL),
-         ("naive", oracle.MODE_NAIVE)]
+         ("naive", oracle.MODE_NAIVE), ("yac", oracle.MODE_YAC), ("base", oracle.MODE_BASE),
+         ("naive_kahan", oracle.MODE_NAIVE_KAHAN)]
 NTHREADS = 16
 
 
