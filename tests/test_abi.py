@@ -63,7 +63,7 @@ def test_invalid_arguments_rejected_without_launch(lib):
     P = lambda x: x.ctypes.data  # noqa: E731
     assert _call(lib, P(a), P(b), P(z), -1, n, P(out), P(cnt), 1) == sgi.SGI_E_INVALID
     assert _call(lib, P(a), P(b), P(z), n, n - 1, P(out), P(cnt), 1) == sgi.SGI_E_INVALID
-    assert _call(lib, P(a), P(b), P(z), n, n, P(out), P(cnt), 3) == sgi.SGI_E_INVALID
+    assert _call(lib, P(a), P(b), P(z), n, n, P(out), P(cnt), 6) == sgi.SGI_E_INVALID
     assert _call(lib, P(a), P(b), P(z), n, n, P(out), P(cnt), -1) == sgi.SGI_E_INVALID
     assert _call(lib, None, P(b), P(z), n, n, P(out), P(cnt), 1) == sgi.SGI_E_INVALID
     assert "null" in sgi.last_error()
