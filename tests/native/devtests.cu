@@ -34,9 +34,12 @@ __device__ bool same_bits_or_zero(double a, double b) {
 
 // out[0]: two_sum value mismatches; out[1]: zero-sign-only differences; out[2]: exactness
 // failures (e != a + b - s checked with a second TwoSum); out[3]: div mismatches (guard ok);
-// out[4]: div guard failures; out[5]: sqrt mismatches (guard ok); out[6]: sqrt guard failures
+// out[4]: div guard failures; out[5]: sqrt mismatches (guard ok); out[6]: sqrt guard failures;
+// out[7]: AccuDOP renormalisation, FastTwoSum(hi, lo) != Knuth TwoSum(hi, lo) (values);
+// out[8]: AccuDOP quadruples that cancelled (Sterbenz case exercised); out[9]: is_zero /
+// is_pos / is_neg / is_nonneg disagreeing with the double comparisons
 extern "C" __global__ void devtest_kernel(uint64_t seed, int64_t n, unsigned long long* out) {
-  unsigned long long c[7] = {0, 0, 0, 0, 0, 0, 0};
+  unsigned long long c[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     uint64_t k = seed * 0x100000001b3ull + (uint64_t)i * 8;
@@ -68,13 +71,37 @@ extern "C" __global__ void devtest_kernel(uint64_t seed, int64_t n, unsigned lon
     double r = sgi::sqrt_fast(sx, oks);
     if (!oks) c[6]++;
     else if (!same_bits_or_zero(r, __dsqrt_rn(sx))) c[5]++;
+    // AccuDOP a*b - c*d and its renormalisation (sgi_query.cuh accux_edge): c*d near a*b
+    {
+      double pa = rnd(k + 11, -100, 100), pb = rnd(k + 12, -100, 100);
+      double pc = rnd(k + 13, -100, 100), pd;
+      uint64_t m2 = mix(k + 14) % 4;
+      if (m2 == 0 || pc == 0.0) pd = rnd(k + 15, -100, 100);
+      else if (m2 == 1) pd = __ddiv_rn(__dmul_rn(pa, pb), pc);            // near-exact cancel
+      else if (m2 == 2) pd = __dadd_rn(__ddiv_rn(__dmul_rn(pa, pb), pc),  // a few ulps off
+                                       __dmul_rn(rnd(k + 16, -56, -50), __ddiv_rn(__dmul_rn(pa, pb), pc)));
+      else pd = __dmul_rn(__ddiv_rn(__dmul_rn(pa, pb), pc), 0.5 + (double)(mix(k + 17) & 7) * 0.25);
+      sgi::dd h = sgi::accu_dop(pa, pb, pc, pd);
+      sgi::dd f = sgi::fast_two_sum(h.hi, h.lo), g = sgi::two_sum_knuth(h.hi, h.lo);
+      if (f.hi != g.hi || f.lo != g.lo) c[7]++;
+      const double p1 = __dmul_rn(pa, pb), p2 = __dmul_rn(pc, pd);
+      if (p1 != 0.0 && p1 == __dadd_rn(__dsub_rn(p1, p2), p2) && fabs(p2) <= 2 * fabs(p1) &&
+          fabs(p1) <= 2 * fabs(p2)) c[8]++;
+      // sign / zero helpers against the double comparisons on the same spread of values
+      const double v[4] = {h.hi, h.lo, a, -b};
+      for (int j = 0; j < 4; ++j) {
+        const double x = v[j];
+        if (sgi::is_zero(x) != (x == 0.0) || sgi::is_pos(x) != (x > 0.0) ||
+            sgi::is_neg(x) != (x < 0.0) || sgi::is_nonneg(x) != (x >= 0.0)) c[9]++;
+      }
+    }
   }
-  for (int j = 0; j < 7; ++j)
+  for (int j = 0; j < 10; ++j)
     if (c[j]) atomicAdd(out + j, c[j]);
 }
 
 extern "C" int sgi_devtest(uint64_t seed, int64_t n, unsigned long long* d_out) {
-  cudaMemset(d_out, 0, 7 * sizeof(unsigned long long));
+  cudaMemset(d_out, 0, 10 * sizeof(unsigned long long));
   devtest_kernel<<<148 * 8, 256>>>(seed, n, d_out);
   return cudaDeviceSynchronize() == cudaSuccess ? 0 : 1;
 }

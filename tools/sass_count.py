@@ -17,4 +17,4 @@ for block in re.split(r"\n\s+Function : ", txt)[1:]:
     fp64 = sum(body[k] for k in FP64)
     short = re.sub(r"_ZN\d+_GLOBAL__N__\w+?\d+(sgi_\w+?)I?L?i?(\d)?E.*", r"\1<\2>", name)
     print(f"{short[:60]:60s} body={sum(body.values()):5d} FP64={fp64:4d} "
-          + " ".join(f"{k}={body[k]}" for k in (*FP64, "MUFU", "FSETP", "ISETP", "SEL", "LDG", "STG", "BRA", "CALL") if body[k]))
+          + " ".join(f"{k}={body[k]}" for k in (*FP64, "MUFU", "FSETP", "FSEL", "SEL", "PLOP3", "LOP3", "IMAD", "IADD3", "ISETP", "LDS", "LDG", "STG", "BRA", "CALL") if body[k]))

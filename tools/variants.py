@@ -17,12 +17,9 @@ OUT = os.path.join(ROOT, "build", "variants")
 
 VARIANTS = {
     "base": {},
-    "e512_s2": {'SGI_EFT_STAGES': 2},
-    "e512_s4": {'SGI_EFT_STAGES': 4},
-    "e512_s5": {'SGI_EFT_STAGES': 5},
-    "e512_s6": {'SGI_EFT_STAGES': 6},
-    "e256_s6": {'SGI_EFT_THREADS': 256, 'SGI_EFT_STAGES': 6},
-    "e384_s5": {'SGI_EFT_THREADS': 384, 'SGI_EFT_STAGES': 5},
+    "knuth": {'SGI_TS_KNUTH': 1},
+    "e768_s3": {'SGI_EFT_THREADS': 768},
+    "e1024_s3": {'SGI_EFT_THREADS': 1024},
 }
 
 
@@ -40,7 +37,7 @@ def build():
         print(name, regs[:6])
 
 
-def time_all(n, rounds=7, reps=20):
+def time_all(n, rounds=7, reps=20, config=2):
     """Interleaved timing: every round times every (variant, mode) once, so clock drift hits
     all variants alike; reports the median over rounds and the SM clock seen (NVML)."""
     import statistics
@@ -57,7 +54,7 @@ def time_all(n, rounds=7, reps=20):
     a = torch.empty((3, n), dtype=torch.float64, device=dev)
     b = torch.empty_like(a)
     z0 = torch.empty(n, dtype=torch.float64, device=dev)
-    sgi_inputs.generate_device(2, n, a, b, z0)
+    sgi_inputs.generate_device(config, n, a, b, z0, seed=config)
     out = torch.empty((2, 3, n), dtype=torch.float64, device=dev)
     cnt = torch.empty(n, dtype=torch.uint8, device=dev)
     st = torch.cuda.current_stream()
@@ -110,8 +107,9 @@ if __name__ == "__main__":
     if sys.argv[1] == "build":
         build()
     else:
-        n = int(sys.argv[3]) if len(sys.argv) > 3 else 1 << 24
-        rows = time_all(n)
+        n = int(sys.argv[3]) if len(sys.argv) > 3 and sys.argv[2] == "--n" else 1 << 24
+        cfg = int(sys.argv[sys.argv.index("--config") + 1]) if "--config" in sys.argv else 2
+        rows = time_all(n, config=cfg)
         os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
         with open(os.path.join(ROOT, "gpurun_out", "variants.json"), "w") as fh:
             json.dump(rows, fh, indent=1)
