@@ -16,10 +16,10 @@ sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "build", "variants")
 
 VARIANTS = {
-    "base": {},
-    "knuth": {'SGI_TS_KNUTH': 1},
-    "e768_s3": {'SGI_EFT_THREADS': 768},
-    "e1024_s3": {'SGI_EFT_THREADS': 1024},
+    "base": {'SGI_DBG_CLOCK': 1},
+    "pair_t512": {'SGI_EFT_PAIR': 1, 'SGI_DBG_CLOCK': 1},
+    "nostore": {'SGI_DBG_NOSTORE': 1, 'SGI_DBG_CLOCK': 1},
+    "noload_nostore": {'SGI_DBG_NOLOAD': 1, 'SGI_DBG_NOSTORE': 1, 'SGI_DBG_CLOCK': 1},
 }
 
 
@@ -58,9 +58,10 @@ def time_all(n, rounds=7, reps=20, config=2):
     out = torch.empty((2, 3, n), dtype=torch.float64, device=dev)
     cnt = torch.empty(n, dtype=torch.uint8, device=dev)
     st = torch.cuda.current_stream()
-    fns = {}
+    fns, libs = {}, {}
     for name in VARIANTS:
         L = ctypes.CDLL(os.path.join(OUT, f"libsgi_{name}.so"))
+        libs[name] = L
         f = L.sgi_intersect_arc_lat
         f.restype = ctypes.c_int
         f.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int64] * 2 + [ctypes.c_void_p] * 2 + \
@@ -68,6 +69,7 @@ def time_all(n, rounds=7, reps=20, config=2):
         fns[name] = f
     modes = (1,)
     times = {(v, m): [] for v in VARIANTS for m in modes}
+    eff = {(v, m): [] for v in VARIANTS for m in modes}
     clocks = []
     ref = {}
     same = {}
@@ -86,6 +88,11 @@ def time_all(n, rounds=7, reps=20, config=2):
                 torch.cuda.synchronize()
                 clocks.append(clock())
                 times[(name, mode)].append(e0.elapsed_time(e1) / reps)
+                if hasattr(libs[name], "sgi_dbg_clock"):
+                    buf = (ctypes.c_longlong * 2)()
+                    libs[name].sgi_dbg_clock(buf)
+                    if buf[1] > 0:
+                        eff[(name, mode)].append(buf[0] / buf[1] * 1e3)
                 if r == 0:
                     if mode not in ref:
                         ref[mode] = (out.clone(), cnt.clone())
@@ -96,7 +103,9 @@ def time_all(n, rounds=7, reps=20, config=2):
         med = statistics.median(ts)
         rows.append({"variant": name, "mode": mode, "ms_median": round(med, 4),
                      "ms_min": round(min(ts), 4), "Garcs_s": round(n / med / 1e6, 2),
-                     "bitwise_same_as_base": same[(name, mode)]})
+                     "bitwise_same_as_base": same[(name, mode)],
+                     "cta0_clock_mhz": round(statistics.median(eff[(name, mode)]), 1)
+                     if eff[(name, mode)] else None})
         print(json.dumps(rows[-1]), flush=True)
     print(json.dumps({"sm_clock_mhz_min": min(clocks), "sm_clock_mhz_median":
                       statistics.median(clocks), "sm_clock_mhz_max": max(clocks)}))
