@@ -32,11 +32,13 @@ BYTES_PER_ARC = 56 + 48 + 1          # a, b, z0 in; two xyz slots + uint8 count 
 # Algorithmic FP64 operations per query (add/sub/mul/fma/div/sqrt = 1 each) of the op sequence
 # in csrc/sgi_query.cuh; derivation in DESIGN.md §5.
 FP64_OPS = {"eft": 362, "eft_literal": 347, "naive": 42, "yac": 48, "base": 47, "naive_kahan": 45}
-SEEDS = {2: 2, 3: 3, 5: 5}
+SEEDS = {2: 2, 3: 3, 5: 5, 6: 6, 7: 7}
 CONFIG_DESC = {
     2: "C2 short arcs (midpoint uniform, length log-uniform [1e-4,1e-2] rad, z0 between endpoint z)",
     3: "C3 ill-conditioned arcs (near-tangent / near-polar / near-coincident thirds)",
     5: "C5 mixed arcs (50% C1, 25% C2, 25% uniform endpoints with z0 uniform in [-1,1])",
+    6: "paper primary accuracy dataset (P:949): 17 latitude bands, z0 between endpoint z",
+    7: "paper secondary dataset (P:951-953): shallow near-equator arcs, z0 = circle top - r",
 }
 
 
@@ -47,7 +49,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--mode", default="eft",
                    choices=["eft", "eft_literal", "naive", "yac", "base", "naive_kahan"])
-    p.add_argument("--config", type=int, default=2, choices=[2, 3, 5])
+    p.add_argument("--config", type=int, default=2, choices=[2, 3, 5, 6, 7])
     p.add_argument("--n", type=int, default=1 << 24, help="arcs per rank")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--e2e-steps", type=int, default=5)

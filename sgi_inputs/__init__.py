@@ -10,6 +10,9 @@ Configs (BASELINE.json ``configs``, recipe in DESIGN.md §3):
   3  C3  2^24 ill-conditioned arcs: near-tangent / near-polar / near-coincident (seed 3)
   4  C4  cubed-sphere ne=1024 edges x 1,800 latitudes, zonal-mean pairing      (numpy, host)
   5  C5  2^30 mixed arcs, sharded by global index                              (seed 5)
+  6  the paper's primary accuracy dataset: 17 latitude bands, arc i in band i % 17 (seed 6)
+  7  the paper's secondary dataset: 13 decades of the offset r, arc i in decade
+     i % 13                                                                     (seed 7)
 """
 from __future__ import annotations
 
@@ -24,9 +27,30 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 HOST_LIB = os.path.join(_HERE, "libsgi_gen_host.so")
 DEV_LIB = os.path.join(_HERE, "libsgi_gen_dev.so")
 
-CONFIG_SIZES = {1: 10_000, 2: 1 << 24, 3: 1 << 24, 5: 1 << 30}
-CONFIG_SEEDS = {1: 0, 2: 2, 3: 3, 4: 4, 5: 5}
+CONFIG_SIZES = {1: 10_000, 2: 1 << 24, 3: 1 << 24, 5: 1 << 30, 6: 17 << 16, 7: 13 << 16}
+CONFIG_SEEDS = {1: 0, 2: 2, 3: 3, 4: 4, 5: 5, 6: 6, 7: 7}
 C3_CLASSES = ("near-tangent", "near-polar", "near-coincident")
+# gen.h gen_band_edge(): latitude band edges in degrees of the primary dataset (SPEC S:506's
+# default schedule; the paper does not print its own), and the secondary dataset's r decades
+PRIMARY_BAND_EDGES = (0.0, 1e-4, 1e-3, 1e-2, 0.1, 1.0, 11.0, 21.0, 31.0, 41.0, 51.0, 61.0, 71.0,
+                      81.0, 89.0, 89.9, 89.99, 89.999)
+SECONDARY_DECADES = tuple((10.0 ** (d - 15), 10.0 ** (d - 14)) for d in range(13))
+
+
+def group_of(config: int, index):
+    """Band (config 6) or r decade (config 7) of global arc index (scalar or array)."""
+    if config == 6:
+        return index % (len(PRIMARY_BAND_EDGES) - 1)
+    if config == 7:
+        return index % len(SECONDARY_DECADES)
+    raise ValueError(f"config {config} has no groups")
+
+
+def group_label(config: int, g: int) -> str:
+    if config == 6:
+        return f"lat ({PRIMARY_BAND_EDGES[g]:g}, {PRIMARY_BAND_EDGES[g + 1]:g}] deg"
+    lo, hi = SECONDARY_DECADES[g]
+    return f"r [{lo:.0e}, {hi:.0e})"
 
 
 def _newer(target: str, *sources: str) -> bool:
@@ -83,7 +107,7 @@ def _dev_lib():
 
 def generate_host(config: int, n: int, offset: int = 0, seed: int | None = None,
                   ld: int | None = None):
-    """Arcs [offset, offset+n) of `config` (1, 2, 3 or 5) on the host.
+    """Arcs [offset, offset+n) of `config` (1, 2, 3, 5, 6 or 7) on the host.
 
     Returns (a, b, z0) as float64 arrays of shapes (3, ld), (3, ld), (ld,); columns >= n are 0.
     """

@@ -1,4 +1,5 @@
-/* sgi_inputs/gen.h — seeded, counter-based synthetic arc generators (configs C1-C3, C5).
+/* sgi_inputs/gen.h — seeded, counter-based synthetic arc generators (configs C1-C3, C5, and
+ * the paper's primary / secondary accuracy datasets, configs 6 and 7).
  *
  * A module of its own: it builds INPUTS only (endpoint pairs a, b and latitude z0) and holds
  * none of the method's arithmetic (no AccuX, no EFT, no intersection formula).  The same source
@@ -179,8 +180,52 @@ GEN_HD void gen_short_arc(const double m[3], const double d[3], double h, double
   gen_normalize3(b);
 }
 
+/* sin and cos of x in [-4, 8] (radians) from +,-,*,/ only: Cody-Waite reduction by pi/2 to
+ * |r| <= pi/4 (two-part pi/2), Taylor series to degree 23/22, quadrant rotation.  Accuracy
+ * ~1 ulp — irrelevant for a sampler (inputs need not be unit length); what matters
+ * is that host and device evaluate the identical op sequence. */
+GEN_HD void gen_sincos(double x, double* sn, double* cs) {
+  double kq = (double)(int64_t)GEN_ADD(GEN_MUL(x, 0.6366197723675814), 8.5);  /* round(x*2/pi)+8 */
+  kq = GEN_SUB(kq, 8.0);
+  double r = GEN_SUB(GEN_SUB(x, GEN_MUL(kq, 1.5707963267948966)), GEN_MUL(kq, 6.123233995736766e-17));
+  double r2 = GEN_MUL(r, r);
+  double ps = 1.0, pc = 1.0;
+  for (int k = 23; k >= 3; k -= 2) ps = GEN_SUB(1.0, GEN_DIV(GEN_MUL(ps, r2), (double)(k * (k - 1))));
+  for (int k = 22; k >= 2; k -= 2) pc = GEN_SUB(1.0, GEN_DIV(GEN_MUL(pc, r2), (double)(k * (k - 1))));
+  double s0 = GEN_MUL(r, ps), c0 = pc;
+  int q = ((int)kq) & 3;
+  if (q == 0) { *sn = s0; *cs = c0; }
+  else if (q == 1) { *sn = c0; *cs = -s0; }
+  else if (q == 2) { *sn = -s0; *cs = -c0; }
+  else { *sn = -c0; *cs = s0; }
+}
+
+#define GEN_DEG 0.017453292519943295   /* pi/180 */
+
+/* Point at latitude lat_deg in [0, 90] and longitude lon_deg: z = cos(colatitude) and
+ * |p_xy| = sin(colatitude), with the colatitude 90 - lat formed exactly near the pole. */
+GEN_HD void gen_latlon(double lat_deg, double lon_deg, double p[3]) {
+  double sc, cc, sl, cl;
+  gen_sincos(GEN_MUL(GEN_SUB(90.0, lat_deg), GEN_DEG), &sc, &cc);
+  gen_sincos(GEN_MUL(lon_deg, GEN_DEG), &sl, &cl);
+  p[0] = GEN_MUL(sc, cl); p[1] = GEN_MUL(sc, sl); p[2] = cc;
+}
+
+/* The paper's primary accuracy dataset: northern-hemisphere latitude bands, narrower
+ * near the equator and the pole.  The paper does not print its band edges; these are SPEC's
+ * default schedule, in degrees: 17 bands. */
+#define GEN_NBANDS 17
+GEN_HD double gen_band_edge(int k) {
+  const double e[GEN_NBANDS + 1] = {0.0, 1e-4, 1e-3, 1e-2, 0.1, 1.0, 11.0, 21.0, 31.0, 41.0, 51.0,
+                                    61.0, 71.0, 81.0, 89.0, 89.9, 89.99, 89.999};
+  return e[k];
+}
+/* The paper's secondary dataset groups by the decade of the offset r: 13 decades
+ * [1e-15, 1e-14) ... [1e-3, 1e-2). */
+#define GEN_NDECADES 13
+
 /* ------------------------------------------------------------------ configs */
-enum { GEN_C1 = 1, GEN_C2 = 2, GEN_C3 = 3, GEN_C5 = 5 };
+enum { GEN_C1 = 1, GEN_C2 = 2, GEN_C3 = 3, GEN_C5 = 5, GEN_PRIMARY = 6, GEN_SECONDARY = 7 };
 
 /* C1: a, b i.i.d. uniform on the sphere; z0 uniform between a_z and b_z. */
 GEN_HD void gen_arc_uniform(gen_stream* s, double a[3], double b[3], double* z0) {
@@ -260,6 +305,61 @@ GEN_HD void gen_arc_free(gen_stream* s, double a[3], double b[3], double* z0) {
   *z0 = GEN_SUB(GEN_MUL(2.0, gen_uniform(s)), 1.0);
 }
 
+/* Primary dataset, band k = i mod 17: both endpoints at latitudes uniform in the band
+ * and longitudes uniform in [0, 360) degrees; z0 uniform between the endpoint z values. */
+GEN_HD void gen_arc_primary(gen_stream* s, uint64_t i, double a[3], double b[3], double* z0) {
+  const int k = (int)(i % GEN_NBANDS);
+  const double lo = gen_band_edge(k), hi = gen_band_edge(k + 1);
+  const double w = GEN_SUB(hi, lo);
+  double la = GEN_ADD(lo, GEN_MUL(gen_uniform(s), w)), lb = GEN_ADD(lo, GEN_MUL(gen_uniform(s), w));
+  if (la <= 0.0) la = hi;      /* the band is (lo, hi]: u = 0 maps to its top */
+  if (lb <= 0.0) lb = hi;
+  gen_latlon(la, GEN_MUL(360.0, gen_uniform(s)), a);
+  gen_latlon(lb, GEN_MUL(360.0, gen_uniform(s)), b);
+  *z0 = gen_z0_between(s, a[2], b[2]);
+}
+
+/* Secondary dataset, decade d = i mod 13: shallow arcs near the equator, endpoints
+ * in the latitude band (0, 1e-4 deg], and z0 = (top of the great circle) - r with r
+ * log-uniform in [10^(d-15), 10^(d-14)).  Built from a designed circle, so no intersection
+ * arithmetic runs here (reading R10): its top height h = sin(tau) is log-uniform in
+ * [h0, 10 h0], h0 = max(sin(1e-4 deg), 2r) (the circle must reach above z0 = h - r > -h);
+ * apex A = (cos tau cos lam, cos tau sin lam, h), horizontal tangent T = (-sin lam, cos lam, 0);
+ * each endpoint c A -+ sqrt(1 - c^2) T sits on either side of the apex at height z = c h drawn
+ * uniform in (0, min(sin(1e-4 deg), z0 (1 - 1e-3))], so both intersection points lie on the
+ * arc.  z0 uses the designed h, not a height recomputed from the rounded endpoints. */
+GEN_HD void gen_arc_secondary(gen_stream* s, uint64_t i, double a[3], double b[3], double* z0) {
+  const int d = (int)(i % GEN_NDECADES);
+  const double r = gen_logu(s, (double)(d - 15), (double)(d - 14));
+  const double zband = 1.7453292519057202e-06;          /* sin(1e-4 deg) */
+  const double h0 = GEN_MUL(2.0, r) > zband ? GEN_MUL(2.0, r) : zband;
+  const double top = GEN_MUL(h0, gen_exp10(gen_uniform(s)));   /* log-uniform in [h0, 10 h0) */
+  const double ct = GEN_SQRT(GEN_MUL(GEN_SUB(1.0, top), GEN_ADD(1.0, top)));
+  double sl, cl;
+  gen_sincos(GEN_MUL(GEN_MUL(360.0, gen_uniform(s)), GEN_DEG), &sl, &cl);
+  const double A[3] = {GEN_MUL(ct, cl), GEN_MUL(ct, sl), top};
+  const double T[3] = {-sl, cl, 0.0};
+  *z0 = GEN_SUB(top, r);
+  double zmax = GEN_MUL(*z0, 0.999);
+  if (zmax > zband) zmax = zband;
+  for (int e = 0; e < 2; ++e) {
+    double u = gen_uniform(s);
+    double z = GEN_MUL(GEN_SUB(1.0, u), zmax);         /* (0, zmax] */
+    double c = GEN_DIV(z, top);
+    double sn = GEN_SQRT(GEN_MUL(GEN_SUB(1.0, c), GEN_ADD(1.0, c)));
+    double* p = e == 0 ? a : b;
+    double sg = e == 0 ? -1.0 : 1.0;
+    for (int k = 0; k < 3; ++k) p[k] = GEN_ADD(GEN_MUL(c, A[k]), GEN_MUL(GEN_MUL(sg, sn), T[k]));
+  }
+}
+
+/* Group of arc i in the paper-shaped configs: band (primary) or decade (secondary). */
+GEN_HD int gen_group(int config, uint64_t i) {
+  if (config == GEN_PRIMARY) return (int)(i % GEN_NBANDS);
+  if (config == GEN_SECONDARY) return (int)(i % GEN_NDECADES);
+  return 0;
+}
+
 /* Arc `i` (global index) of `config`.  Returns 0 on success, -1 for an unknown config. */
 GEN_HD int gen_arc(int config, uint64_t seed, uint64_t i, double a[3], double b[3], double* z0) {
   gen_stream s;
@@ -279,6 +379,8 @@ GEN_HD int gen_arc(int config, uint64_t seed, uint64_t i, double a[3], double b[
         case 2: gen_arc_short(&s, a, b, z0); return 0;
         default: gen_arc_free(&s, a, b, z0); return 0;
       }
+    case GEN_PRIMARY: gen_arc_primary(&s, i, a, b, z0); return 0;
+    case GEN_SECONDARY: gen_arc_secondary(&s, i, a, b, z0); return 0;
     default: return -1;
   }
 }

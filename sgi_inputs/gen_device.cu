@@ -21,7 +21,7 @@ __global__ void sgi_gen_kernel(int config, uint64_t seed, int64_t offset, int64_
 extern "C" int sgi_gen_device(int config, uint64_t seed, int64_t offset, int64_t n, int64_t ld,
                               double* a, double* b, double* z0, void* stream) {
   if (n < 0 || ld < n || offset < 0) return 1;
-  if (config != GEN_C1 && config != GEN_C2 && config != GEN_C3 && config != GEN_C5) return 1;
+  if ((config < GEN_C1 || config > GEN_SECONDARY || config == 4)) return 1;
   if (n == 0) return 0;
   if (!a || !b || !z0) return 1;
   int dev = 0, sms = 148;

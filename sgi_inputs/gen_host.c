@@ -7,7 +7,7 @@
 int sgi_gen_host(int config, uint64_t seed, int64_t offset, int64_t n, int64_t ld,
                  double* a, double* b, double* z0) {
   if (n < 0 || ld < n || offset < 0) return 1;
-  if (config != GEN_C1 && config != GEN_C2 && config != GEN_C3 && config != GEN_C5) return 1;
+  if ((config < GEN_C1 || config > GEN_SECONDARY || config == 4)) return 1;
   if (n > 0 && (!a || !b || !z0)) return 1;
 #pragma omp parallel for schedule(static)
   for (int64_t j = 0; j < n; ++j) {

@@ -50,7 +50,7 @@ def _build():
 
 
 # ------------------------------------------------------------------ device generator == host
-@pytest.mark.parametrize("config", [1, 2, 3, 5])
+@pytest.mark.parametrize("config", [1, 2, 3, 5, 6, 7])
 def test_device_generator_matches_host(config):
     n = 100_003
     a, b, z = sgi_inputs.generate_host(config, n, offset=12345)
