@@ -114,6 +114,35 @@ sgi_status sgi_zonal_intersect(const double* va, const double* vb, int64_t n_edg
                                size_t work_bytes, int mode, void* stream);
 size_t sgi_zonal_workspace_bytes(int64_t n_edges);
 
+/* Appendix-A instrumentation (Appendix A: "we recorded these results as
+ * pairs of doubles (the leading term and compensation term)").  For each query i, every
+ * intermediate of the mode's op sequence — computed with the IEEE intrinsics, i.e. the values
+ * sgi_intersect_arc_lat reproduces — is written to out_trace[f * ld + i] for the
+ * SGI_TRACE_FIELDS fields f below, and the count to out_count[i].  In the EFT modes each
+ * (hi, lo) pair is the pair AccuX holds: the normal after AccuDOP (and the
+ * renormalisation of SGI_MODE_EFT), |n_xy|^2 and |n|^2 (SumOfSquaresC), z0^2 (TwoProd),
+ * |n|^2 z0^2 (CompDotC), s^2, s (AccSqrt), n_x n_z and n_y n_z, the four numerators after
+ * CompDot's final rounding and as CompDotC pairs before it, and both points.  The plain
+ * binary64 modes fill their own values (lo = 0; unused fields 0; Eq.YAC/BASE numerators use
+ * the normalised normal).  Points are both roots of the great circle, before containment.
+ * Device pointers, one launch on `stream`; a debug path, not tuned.  Errors as for
+ * sgi_intersect_arc_lat (out_trace must not overlap the inputs). */
+#define SGI_TRACE_FIELDS 38
+enum {
+  SGI_TRACE_NX, SGI_TRACE_EX, SGI_TRACE_NY, SGI_TRACE_EY, SGI_TRACE_NZ, SGI_TRACE_EZ,
+  SGI_TRACE_S2, SGI_TRACE_S2_LO, SGI_TRACE_S3, SGI_TRACE_S3_LO, SGI_TRACE_C, SGI_TRACE_C_LO,
+  SGI_TRACE_D, SGI_TRACE_D_LO, SGI_TRACE_SIGMA, SGI_TRACE_SIGMA_LO, SGI_TRACE_S, SGI_TRACE_S_LO,
+  SGI_TRACE_FX, SGI_TRACE_FX_LO, SGI_TRACE_FY, SGI_TRACE_FY_LO,
+  SGI_TRACE_XP, SGI_TRACE_YP, SGI_TRACE_XM, SGI_TRACE_YM,
+  SGI_TRACE_PPX, SGI_TRACE_PPY, SGI_TRACE_PMX, SGI_TRACE_PMY,
+  SGI_TRACE_XP_PAIR, SGI_TRACE_XP_PAIR_LO, SGI_TRACE_YP_PAIR, SGI_TRACE_YP_PAIR_LO,
+  SGI_TRACE_XM_PAIR, SGI_TRACE_XM_PAIR_LO, SGI_TRACE_YM_PAIR, SGI_TRACE_YM_PAIR_LO
+};
+sgi_status sgi_intersect_trace(const double* a, const double* b, const double* z0, int64_t n,
+                               int64_t ld, double* out_trace, uint8_t* out_count, int mode,
+                               void* stream);
+int sgi_trace_fields(void);                                    /* SGI_TRACE_FIELDS */
+
 const char* sgi_status_str(sgi_status s);
 const char* sgi_last_error(void);
 int sgi_abi_version(void);

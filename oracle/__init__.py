@@ -27,7 +27,8 @@ DEGENERATE = 0xFF
 
 TRACE_FIELDS = ("nx", "ex", "ny", "ey", "nz", "ez", "S2", "s2", "S3", "s3", "C", "eC", "D", "eD",
                 "sh", "sl", "s", "es", "Fx", "eFx", "Fy", "eFy", "Xp", "Yp", "Xm", "Ym",
-                "Ppx", "Ppy", "Pmx", "Pmy")
+                "Ppx", "Ppy", "Pmx", "Pmy",
+                "Xp_p", "Xp_s", "Yp_p", "Yp_s", "Xm_p", "Xm_s", "Ym_p", "Ym_s")
 
 PRIM = {"two_sum": 0, "fast_two_sum": 1, "two_prod": 2, "kahan_dop": 3, "accu_dop": 4,
         "sum_non_neg": 5, "sum_of_squares": 6, "sum_of_squares_c": 7, "acc_sqrt": 8,

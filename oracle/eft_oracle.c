@@ -152,6 +152,10 @@ typedef struct {
   double Fx, eFx, Fy, eFy;            /* n_x n_z, n_y n_z */
   double Xp, Yp, Xm, Ym;              /* numerators of both roots */
   double Pp[2], Pm[2];                /* both points' x, y */
+  double Xpp[2], Ypp[2], Xmp[2], Ymp[2]; /* the numerators before CompDot's final rounding: the
+                                          CompDotC pairs (p, sigma) of lines 17/22 (Appendix A
+                                          analyses z0 nx nz + s ny as a pair);
+                                          (value, 0) in the plain-binary64 modes */
 } accux_trace;
 
 /* Alg.8 AccuX, both roots (reading R5). */
@@ -194,6 +198,10 @@ static void accux(const double x1[3], const double x2[3], double z0, int renorm,
   double ym[6] = {Fy1.hi, eFy, nx.hi, nx.lo, nx.hi, nx.lo};
   double Xp = comp_dot(xp, w, 6), Yp = comp_dot(yp, w, 6);
   double Xm = comp_dot(xm, w, 6), Ym = comp_dot(ym, w, 6);
+  pair Xpp = comp_dot_c(xp, w, 6), Ypp = comp_dot_c(yp, w, 6);
+  pair Xmp = comp_dot_c(xm, w, 6), Ymp = comp_dot_c(ym, w, 6);
+  t->Xpp[0] = Xpp.hi; t->Xpp[1] = Xpp.lo; t->Ypp[0] = Ypp.hi; t->Ypp[1] = Ypp.lo;
+  t->Xmp[0] = Xmp.hi; t->Xmp[1] = Xmp.lo; t->Ymp[0] = Ymp.hi; t->Ymp[1] = Ymp.lo;
   /* lines 23-25 */
   t->Pp[0] = -(Xp / S2.hi); t->Pp[1] = -(Yp / S2.hi);
   t->Pm[0] = -(Xm / S2.hi); t->Pm[1] = -(Ym / S2.hi);
@@ -219,6 +227,7 @@ static void naive(const double x1[3], const double x2[3], double z0, accux_trace
   memset(t, 0, sizeof(*t));
   t->nx = nx; t->ny = ny; t->nz = nz; t->S2 = S2; t->S3 = S3; t->sh = sh; t->s = s;
   t->Xp = Xp; t->Yp = Yp; t->Xm = Xm; t->Ym = Ym;
+  t->Xpp[0] = Xp; t->Ypp[0] = Yp; t->Xmp[0] = Xm; t->Ymp[0] = Ym;
   t->Pp[0] = -(Xp / S2); t->Pp[1] = -(Yp / S2);
   t->Pm[0] = -(Xm / S2); t->Pm[1] = -(Ym / S2);
 }
@@ -258,6 +267,7 @@ static void variant(int mode, const double x1[3], const double x2[3], double z0,
   double Xp = bx + (s * uy), Xm = bx - (s * uy);
   double Yp = by - (s * ux), Ym = by + (s * ux);
   t->sh = sh; t->s = s; t->Xp = Xp; t->Yp = Yp; t->Xm = Xm; t->Ym = Ym;
+  t->Xpp[0] = Xp; t->Ypp[0] = Yp; t->Xmp[0] = Xm; t->Ymp[0] = Ym;
   t->Pp[0] = -(Xp / den); t->Pp[1] = -(Yp / den);
   t->Pm[0] = -(Xm / den); t->Pm[1] = -(Ym / den);
   *hx = nx == 0.0 ? 0.0 : ux;
@@ -342,7 +352,7 @@ int oracle_intersect_batch(int mode, const double* a, const double* b, const dou
   return 0;
 }
 
-/* Every intermediate of one query (Appendix-A instrumentation).  Fills 30 doubles
+/* Every intermediate of one query (Appendix-A instrumentation).  Fills 38 doubles
  * in the field order of accux_trace and returns the count. */
 int oracle_trace(int mode, const double x1[3], const double x2[3], double z0, double* out30) {
   accux_trace t;

@@ -9,6 +9,7 @@ Public API (same names as the C ABI):
     intersect_arc_lat_host(a, b, z0, mode="eft", out_xyz=None, out_count=None, work=None, ...)
     count_histogram(out_count, n=None, hist=None, stream=None)
     zonal_intersect(va, vb, lat_z0, mode="eft", cap=None, stream=None)
+    intersect_trace(a, b, z0, mode="eft", n=None, stream=None)   (Appendix-A intermediates)
     host_workspace_bytes(chunk), abi_version(), status_str(code), last_error()
 Layout: a[3, ld], b[3, ld], z0[ld] float64; out_xyz[2, 3, ld] float64; out_count[ld] uint8.
 """
@@ -20,6 +21,11 @@ import os
 from ._build import LIB_PATH, build  # noqa: F401
 
 MODES = {"naive": 0, "eft": 1, "eft_literal": 2, "yac": 3, "base": 4, "naive_kahan": 5}
+# sgi_intersect_trace field order (include/sgi.h SGI_TRACE_*)
+TRACE_FIELDS = ("nx", "ex", "ny", "ey", "nz", "ez", "S2", "s2", "S3", "s3", "C", "eC", "D", "eD",
+                "sh", "sl", "s", "es", "Fx", "eFx", "Fy", "eFy", "Xp", "Yp", "Xm", "Ym",
+                "Ppx", "Ppy", "Pmx", "Pmy",
+                "Xp_p", "Xp_s", "Yp_p", "Yp_s", "Xm_p", "Xm_s", "Ym_p", "Ym_s")
 DEGENERATE = 0xFF
 SGI_OK, SGI_E_INVALID, SGI_E_CUDA = 0, 1, 2
 
@@ -52,6 +58,10 @@ def _load():
                                           vp, vp, vp, ctypes.c_size_t, ctypes.c_int, vp]
         L.sgi_zonal_workspace_bytes.restype = ctypes.c_size_t
         L.sgi_zonal_workspace_bytes.argtypes = [i64]
+        L.sgi_intersect_trace.restype = ctypes.c_int
+        L.sgi_intersect_trace.argtypes = [vp, vp, vp, i64, i64, vp, vp, ctypes.c_int, vp]
+        L.sgi_trace_fields.restype = ctypes.c_int
+        L.sgi_trace_fields.argtypes = []
         L.sgi_status_str.restype = ctypes.c_char_p
         L.sgi_status_str.argtypes = [ctypes.c_int]
         L.sgi_last_error.restype = ctypes.c_char_p
@@ -124,6 +134,25 @@ def intersect_arc_lat(a, b, z0, mode="eft", out_xyz=None, out_count=None, n=None
                                        _stream_ptr(stream))
     _check(rc, "sgi_intersect_arc_lat")
     return out_xyz, out_count
+
+
+def intersect_trace(a, b, z0, mode="eft", n=None, stream=None):
+    """Appendix-A instrumentation (sgi_intersect_trace): every intermediate of each query ->
+    (trace[len(TRACE_FIELDS), ld] float64 CUDA tensor, out_count[ld] uint8)."""
+    import torch
+    ld = z0.shape[0]
+    n = ld if n is None else n
+    _cuda_f64(a, (3, ld), "a")
+    _cuda_f64(b, (3, ld), "b")
+    _cuda_f64(z0, (ld,), "z0")
+    L = _load()
+    assert L.sgi_trace_fields() == len(TRACE_FIELDS)
+    trace = torch.zeros((len(TRACE_FIELDS), ld), dtype=torch.float64, device=z0.device)
+    cnt = torch.empty(ld, dtype=torch.uint8, device=z0.device)
+    rc = L.sgi_intersect_trace(a.data_ptr(), b.data_ptr(), z0.data_ptr(), n, ld, trace.data_ptr(),
+                               cnt.data_ptr(), _mode(mode), _stream_ptr(stream))
+    _check(rc, "sgi_intersect_trace")
+    return trace, cnt
 
 
 def host_workspace_bytes(chunk: int) -> int:

@@ -1,0 +1,70 @@
+"""Appendix-A instrumentation on the device (sgi_intersect_trace): every one of the
+38 intermediates equals oracle (a)'s trace (IEEE ==, NaN == NaN) in every mode on C1 and on C3's
+ill-conditioned classes, and the per-intermediate mean relative errors over the primary dataset
+reproduce the paper's Appendix-A shape from the GPU's own values."""
+import os
+
+import numpy as np
+import pytest
+
+import appendix_a as aa
+import oracle
+import sgi_inputs
+from helpers import U
+
+torch = pytest.importorskip("torch")
+import paper_2510_09892_b200 as sgi  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+MODES = [("eft", oracle.MODE_EFT), ("eft_literal", oracle.MODE_EFT_LITERAL),
+         ("naive", oracle.MODE_NAIVE), ("yac", oracle.MODE_YAC), ("base", oracle.MODE_BASE),
+         ("naive_kahan", oracle.MODE_NAIVE_KAHAN)]
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def gpu_trace(a, b, z0, mode):
+    da, db, dz = (torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (a, b, z0))
+    tr, cnt = sgi.intersect_trace(da, db, dz, mode=mode)
+    torch.cuda.synchronize()
+    return tr.cpu().numpy(), cnt.cpu().numpy()
+
+
+def test_trace_field_order_matches_oracle():
+    assert sgi.TRACE_FIELDS == oracle.TRACE_FIELDS
+
+
+@pytest.mark.parametrize("config,n", [(1, 10_000), (3, 3 * 2000)])
+@pytest.mark.parametrize("mode,omode", MODES)
+def test_trace_equals_oracle_trace(config, n, mode, omode):
+    a, b, z0 = sgi_inputs.generate_host(config, n)
+    tr, cnt = gpu_trace(a, b, z0, mode)
+    ref = np.zeros_like(tr)
+    rcnt = np.zeros(n, np.uint8)
+    for i in range(n):
+        c, t = oracle.trace(omode, a[:, i], b[:, i], z0[i])
+        ref[:, i] = [t[f] for f in oracle.TRACE_FIELDS]
+        rcnt[i] = c
+    assert np.array_equal(cnt, rcnt)
+    same = (tr == ref) | (np.isnan(tr) & np.isnan(ref))
+    bad = [oracle.TRACE_FIELDS[k] for k in np.nonzero(~same.all(1))[0]]
+    assert not bad, f"fields differing from oracle (a): {bad}"
+
+
+def test_appendix_a_table_from_the_gpu():
+    n = 17 * 300
+    a, b, z0 = sgi_inputs.generate_host(6, n)
+    exacts = [aa.exact_values(a[:, i], b[:, i], z0[i]) for i in range(n)]
+    tables = {}
+    for mode in ("eft", "eft_literal", "naive", "yac", "base"):
+        tr, _ = gpu_trace(a, b, z0, mode)
+        traces = [dict(zip(sgi.TRACE_FIELDS, tr[:, i].tolist())) for i in range(n)]
+        tables[mode] = aa.mean_table(traces, exacts)
+    eft = tables["eft"]
+    for lab, hi, lo, _ in aa.ITEMS:
+        if lo:
+            assert eft[lab][0] < U, (lab, eft[lab])
+    for lab in ("fl(numerator)", "fl(|n_xy|^2)", "p_x"):
+        assert U / 16 <= eft[lab][0] <= 2 * U, (lab, eft[lab])
+    rdir = os.environ.get("SGI_REPORT_DIR", os.path.join(ROOT, "gpurun_out"))
+    aa.write_csv(os.path.join(rdir, "appendix_a_gpu.csv"), tables,
+                 f"sgi_intersect_trace on B200, primary dataset (config 6), {n} queries")
