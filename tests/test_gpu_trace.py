@@ -58,7 +58,10 @@ def test_appendix_a_table_from_the_gpu():
     for mode in ("eft", "eft_literal", "naive", "yac", "base"):
         tr, _ = gpu_trace(a, b, z0, mode)
         traces = [dict(zip(sgi.TRACE_FIELDS, tr[:, i].tolist())) for i in range(n)]
-        tables[mode] = aa.mean_table(traces, exacts)
+        tab = aa.mean_table(traces, exacts)
+        if mode in ("yac", "base"):      # other intermediates are of the normalised formulas
+            tab = {k: v for k, v in tab.items() if k in ("n_x", "|n|^2", "|n_xy|^2", "p_x")}
+        tables[mode] = tab
     eft = tables["eft"]
     for lab, hi, lo, _ in aa.ITEMS:
         if lo:
