@@ -1,27 +1,25 @@
 // sgi_zonal.cu — fused zonal-mean pass: mesh edges x latitude table -> compacted intersections
 // (the paper's motivating application, zonal means on regridding meshes).
 //
-// Every CTA owns one contiguous range of edges (equal sizes, rounded to tiles of kTile edges),
-// and the pass runs as three launches:
-//   count  per edge, from the accurate (AccuDOP) normal rounded once, the arc's z-range: the
+// Three launches over tiles of kEdges consecutive edges:
+//   filter per edge, from the accurate (AccuDOP) normal rounded once, the arc's z-range: the
 //          endpoints' z/|x| and, when the great circle's extremum lies strictly inside the arc
 //          (dz/dt changes sign: g1 = (n x a)_z > 0 > g2 = (n x b)_z for a maximum), the apex
 //          height sqrt(|n_xy|^2/|n|^2); widened by delta = 2^-40 (far above its rounding error);
-//          a binary search in the latitude table (shared memory) gives the candidate latitudes;
-//          each CTA sums its candidates;
-//   scan   one CTA turns the per-CTA sums into output bases (and the total);
-//   emit   each CTA re-walks its range tile by tile: the same filter, plus the query's
-//          z0-independent AccuX head (accurate normal pairs, |n_xy|^2, |n|^2 — lines 2-6,
-//          P:746-750), staged in shared memory with the endpoints; a block scan orders the tile's candidates (edge-major, latitude
-//          ascending, deterministic), and the tile's pairs are processed densely (pair c ->
-//          thread c mod kTile, so lanes are not idle on edges that span no latitude), running the
-//          z0-dependent tail of the query (AccuX lines 7-25 + containment).
-// Edges are read twice (48 B each, 2 x 0.6 GB for the C4 mesh) instead of paying a device-wide
-// decoupled look-back per tile, whose frontier propagation limited a single-pass version to a
-// fraction of this throughput.  A pair's result is bit-identical to
-// sgi_intersect_arc_lat on the same (a, b, z0): head and tail are the same device code.
-// Candidate pairs whose latitude only touches the widened range come out with count 0; every
-// pair with a nonzero count is a candidate (tests/test_gpu_zonal.py).
+//          a search in the latitude table (shared memory) gives the candidate latitudes
+//          [klo, klo + kcnt), stored per edge (8 B) with each tile's candidate sum;
+//   scan   one CTA turns the tile sums into output bases (and the total);
+//   emit   CTAs walk tiles in any order (each tile knows its base): a block scan of the stored
+//          kcnt orders the tile's candidates (edge-major, latitude ascending, deterministic)
+//          and compacts the candidate edges; only those are read again, one per thread, and
+//          get the query's z0-independent AccuX head (accurate normal pairs, |n_xy|^2, |n|^2 —
+//          lines 2-6), staged in shared memory; the tile's pairs are then processed
+//          densely (pair c -> thread c mod kThreads,
+//          so lanes are not idle on edges that span no latitude), running the z0-dependent tail
+//          of the query (AccuX lines 7-25 + containment).
+// A pair's result is bit-identical to sgi_intersect_arc_lat on the same (a, b, z0): head and
+// tail are the same device code.  Candidate pairs whose latitude only touches the widened range
+// come out with count 0; every pair with a nonzero count is a candidate (tests/test_gpu_zonal.py).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -36,9 +34,12 @@ void set_error_msg(const char* msg, cudaError_t e);   // sgi_capi.cu: sgi_last_e
 
 namespace {
 
-constexpr int kTile = 256;                        // threads per CTA = edges per tile
+#ifndef SGI_ZONAL_THREADS
+#define SGI_ZONAL_THREADS 256
+#endif
+constexpr int kThreads = SGI_ZONAL_THREADS;       // threads per CTA
+constexpr int kEdges = 2 * kThreads;              // edges per tile (two adjacent per thread)
 constexpr int kLatSmem = 4096;                    // latitude tables up to this length live in smem
-constexpr int kMaxCtas = 4096;                    // per-CTA sums held in the workspace
 constexpr double kDelta = 9.094947017729282e-13;  // 2^-40
 
 __device__ __forceinline__ int lower_bound(const double* t, int n, double x) {  // first t[k] >= x
@@ -59,10 +60,9 @@ __device__ __forceinline__ int upper_bound(const double* t, int n, double x) {  
   return lo;
 }
 
-struct SmemEdge {   // endpoint coordinates of one staged edge, read by pair threads
-  const double* p;  // 6 doubles, contiguous
-  __device__ __forceinline__ double operator()(int c) const { return p[c]; }
-};
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
 
 struct EdgeX {
   double x[6];
@@ -102,178 +102,318 @@ __device__ __forceinline__ void candidates(const double* x, const double* tab, i
     kcnt = nlat;                                     // n = 0: degenerate at every latitude
   } else if (zhi == zhi && zlo == zlo) {             // NaN inputs: no candidates
     klo = lower_bound(tab, nlat, __dsub_rn(zlo, kDelta));
-    kcnt = upper_bound(tab, nlat, __dadd_rn(zhi, kDelta)) - klo;
+    // the upper end: most edges span 0-2 latitudes, so step forward a few entries before
+    // falling back to a binary search over the rest of the table
+    const double top = __dadd_rn(zhi, kDelta);
+    int khi = klo;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) khi += (khi < nlat && tab[khi] <= top) ? 1 : 0;
+    if (khi < nlat && tab[khi] <= top) khi = khi + upper_bound(tab + khi, nlat - khi, top);
+    kcnt = khi - klo;
   }
-}
-
-__device__ __forceinline__ void cta_range(int64_t ne, int64_t& lo, int64_t& hi) {
-  const int64_t per = ((ne + gridDim.x - 1) / gridDim.x + kTile - 1) / kTile * kTile;
-  lo = (int64_t)blockIdx.x * per;
-  hi = lo + per < ne ? lo + per : ne;
 }
 
 __device__ __forceinline__ const double* stage_lat(double* s_lat, const double* lat, int nlat) {
   if (nlat <= kLatSmem) {
-    for (int k = threadIdx.x; k < nlat; k += kTile) s_lat[k] = lat[k];
+    for (int k = threadIdx.x; k < nlat; k += kThreads) s_lat[k] = lat[k];
     __syncthreads();
     return s_lat;
   }
   return lat;
 }
 
-// Block-wide inclusive scan of one int per thread (kTile threads); returns the inclusive value
-// and leaves the block total in *total.
-__device__ __forceinline__ int block_scan(int v, int* s_warp, int* total) {
+// Block-wide inclusive scan of one 64-bit value per thread (kThreads threads); returns the
+// inclusive value and leaves the block total in *total.
+__device__ __forceinline__ unsigned long long block_scan(unsigned long long v,
+                                                         unsigned long long* s_warp,
+                                                         unsigned long long* total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
-    int y = __shfl_up_sync(0xffffffffu, v, d);
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, v, d);
     if (lane >= d) v += y;
   }
   if (lane == 31) s_warp[warp] = v;
   __syncthreads();
   if (warp == 0) {
-    int w = lane < kTile / 32 ? s_warp[lane] : 0;
+    unsigned long long w = lane < kThreads / 32 ? s_warp[lane] : 0;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, w, d);
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, w, d);
       if (lane >= d) w += y;
     }
-    if (lane < kTile / 32) s_warp[lane] = w;
+    if (lane < kThreads / 32) s_warp[lane] = w;
   }
   __syncthreads();
-  const int incl = v + (warp > 0 ? s_warp[warp - 1] : 0);
-  *total = s_warp[kTile / 32 - 1];
+  const unsigned long long incl = v + (warp > 0 ? s_warp[warp - 1] : 0);
+  *total = s_warp[kThreads / 32 - 1];
   return incl;
 }
 
-// Pass 1: candidate count of every CTA's edge range.
-__global__ void __launch_bounds__(kTile)
-sgi_zonal_count_kernel(const double* __restrict__ va, const double* __restrict__ vb, int64_t ne,
-                       int64_t lde, const double* __restrict__ lat, int nlat,
-                       unsigned long long* __restrict__ cta_sum) {
+// Pass 1: candidate latitudes of every edge, cand[e] = (klo, kcnt), and each tile's sum.
+// Persistent CTAs stride over the tiles (the latitude table is staged once per CTA); thread
+// tid owns edges 2 tid and 2 tid + 1 of a tile, the next tile's loads issued before this one's
+// arithmetic.
+__global__ void __launch_bounds__(kThreads)
+sgi_zonal_filter_kernel(const double* __restrict__ va, const double* __restrict__ vb, int64_t ne,
+                        int64_t lde, const double* __restrict__ lat, int nlat,
+                        int2* __restrict__ cand, unsigned long long* __restrict__ tile_sum) {
   extern __shared__ __align__(16) double s_lat[];
+  __shared__ unsigned long long s_red[kThreads / 32];
   const double* tab = stage_lat(s_lat, lat, nlat);
-  int64_t lo, hi;
-  cta_range(ne, lo, hi);
-  unsigned long long acc = 0;
-  EdgeX cur;
-  int64_t e = lo + threadIdx.x;
-  if (e < hi) load_edge(cur, va, vb, lde, e);
-  for (; e - threadIdx.x < hi; e += kTile) {
-    EdgeX nxt;
-    if (e + kTile < hi) load_edge(nxt, va, vb, lde, e + kTile);
-    if (e < hi) {
-      int klo, kcnt;
-      candidates(cur.x, tab, nlat, klo, kcnt);
-      acc += (unsigned long long)kcnt;
-    }
-    cur = nxt;
-  }
+  const int64_t ntiles = (ne + kEdges - 1) / kEdges;
+  int64_t t = blockIdx.x;
+  EdgeX cur[2];
 #pragma unroll
-  for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
-  __shared__ unsigned long long s_acc;
-  if (threadIdx.x == 0) s_acc = 0;
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) atomicAdd(&s_acc, acc);
-  __syncthreads();
-  if (threadIdx.x == 0) cta_sum[blockIdx.x] = s_acc;
-}
-
-// Pass 2: exclusive scan of the per-CTA sums (one CTA), total to *d_total.
-__global__ void __launch_bounds__(1024)
-sgi_zonal_scan_kernel(unsigned long long* __restrict__ cta_sum, int nctas,
-                      unsigned long long* __restrict__ d_total) {
-  __shared__ unsigned long long s[kMaxCtas];
-  for (int i = threadIdx.x; i < nctas; i += blockDim.x) s[i] = cta_sum[i];
-  __syncthreads();
-  if (threadIdx.x == 0) {                       // <= 4096 entries: a serial scan is ~microseconds
-    unsigned long long run = 0;
-    for (int i = 0; i < nctas; ++i) {
-      const unsigned long long v = s[i];
-      s[i] = run;
-      run += v;
-    }
-    *d_total = run;
+  for (int j = 0; j < 2; ++j) {
+    const int64_t e = t * kEdges + 2 * threadIdx.x + j;
+    if (t < ntiles && e < ne) load_edge(cur[j], va, vb, lde, e);
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < nctas; i += blockDim.x) cta_sum[i] = s[i];
+  for (; t < ntiles; t += gridDim.x) {
+    const int64_t e0 = t * kEdges + 2 * threadIdx.x, en = e0 + (int64_t)gridDim.x * kEdges;
+    EdgeX nxt[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      if (en + j < ne) load_edge(nxt[j], va, vb, lde, en + j);
+    unsigned long long sum = 0;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (e0 + j < ne) {
+        int klo, kcnt;
+        candidates(cur[j].x, tab, nlat, klo, kcnt);
+        cand[e0 + j] = make_int2(klo, kcnt);
+        sum += (unsigned)kcnt;
+      }
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, d);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long acc = 0;
+#pragma unroll
+      for (int w = 0; w < kThreads / 32; ++w) acc += s_red[w];
+      tile_sum[t] = acc;
+    }
+    __syncthreads();
+    cur[0] = nxt[0];
+    cur[1] = nxt[1];
+  }
 }
 
-// Pass 3: emit every candidate pair of the CTA's range at its ordered output slot.
-constexpr size_t kEmitSmem = 0;
+// Pass 2: exclusive scan of the tile sums in place, the total to *d_total (one CTA).  Rounds of
+// kScanRound entries: a coalesced load into shared memory, a serial scan of 4 contiguous
+// entries per thread, a block scan of the thread totals, a coalesced store.
+constexpr int kScanThreads = 1024, kScanPer = 4, kScanRound = kScanThreads * kScanPer;
+__global__ void __launch_bounds__(kScanThreads)
+sgi_zonal_scan_kernel(unsigned long long* __restrict__ tile_sum, int64_t ntiles,
+                      unsigned long long* __restrict__ d_total) {
+  __shared__ unsigned long long s[kScanRound];
+  __shared__ unsigned long long s_warp[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  unsigned long long carry = 0;
+  for (int64_t r0 = 0; r0 < ntiles; r0 += kScanRound) {
+#pragma unroll
+    for (int k = 0; k < kScanPer; ++k) {
+      const int64_t i = r0 + k * kScanThreads + tid;
+      s[k * kScanThreads + tid] = i < ntiles ? tile_sum[i] : 0;
+    }
+    __syncthreads();
+    unsigned long long v[kScanPer], sum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanPer; ++k) {
+      v[k] = s[tid * kScanPer + k];
+      sum += v[k];
+    }
+    unsigned long long x = sum;                      // block scan of the thread totals
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      unsigned long long w = s_warp[lane];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, w, d);
+        if (lane >= d) w += y;
+      }
+      s_warp[lane] = w;
+    }
+    __syncthreads();
+    unsigned long long run = carry + x - sum + (warp > 0 ? s_warp[warp - 1] : 0);
+#pragma unroll
+    for (int k = 0; k < kScanPer; ++k) {
+      s[tid * kScanPer + k] = run;
+      run += v[k];
+    }
+    const unsigned long long round_total = s_warp[31];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kScanPer; ++k) {
+      const int64_t i = r0 + k * kScanThreads + tid;
+      if (i < ntiles) tile_sum[i] = s[k * kScanThreads + tid];
+    }
+    carry += round_total;
+    __syncthreads();
+  }
+  if (tid == 0) *d_total = carry;
+}
+
+// Pass 3: emit every candidate pair of each tile at its ordered output slot.
+//
+// Each tile's endpoint planes and candidate ranges are staged in shared memory by cp.async one
+// tile ahead (double buffer), so the compute never waits on a gather.  A block scan of the
+// stored kcnt compacts the tile's candidate edges in edge order; then, when every candidate
+// spans at most kFuseMax latitudes (the common case: mesh edges are short), one thread per
+// candidate runs the query's z0-independent AccuX head (lines 2-6) once and the z0-dependent
+// tail (lines 7-25 + containment) for each of its latitudes.  Tiles with a long candidate range
+// process their pairs densely instead (pair c -> thread c mod kThreads, head recomputed per
+// pair), so no lane idles behind one long edge.
+constexpr int kFuseMax = 4;
+struct EmitStage {                 // one tile's inputs
+  double x[6][kEdges];             // endpoint planes a_x, a_y, a_z, b_x, b_y, b_z
+  int2 cand[kEdges];               // (klo, kcnt) per edge
+};
+struct EmitList {                  // the tile's compacted candidate edges
+  int edge[kEdges];                // tile-local edge index of candidate c
+  int klo[kEdges];                 // first candidate latitude of candidate c
+  int kcnt[kEdges];                // number of candidate latitudes of candidate c
+  long long off[kEdges];           // first pair of candidate c within the tile
+};
+struct EmitSmem {
+  EmitStage stage[2];
+  EmitList list[2];
+};
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+
+// Thread tid stages edges 2 tid, 2 tid + 1 of tile t (those below ne) and commits the group.
+__device__ __forceinline__ void stage_tile(EmitStage& S, int64_t t, int64_t ne, int64_t lde,
+                                           const double* __restrict__ va,
+                                           const double* __restrict__ vb,
+                                           const int2* __restrict__ cand) {
+  const int l0 = 2 * threadIdx.x;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int64_t e = t * kEdges + l0 + j;
+    if (e < ne) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        cp_async8(&S.x[c][l0 + j], va + c * lde + e);
+        cp_async8(&S.x[3 + c][l0 + j], vb + c * lde + e);
+      }
+      cp_async8(&S.cand[l0 + j], cand + e);
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+template <int MODE, class IN>
+__device__ __forceinline__ void emit_pair(const sgi::EdgePre& pre, const IN& in, int64_t edge,
+                                          int k, const double* tab, int64_t j, int64_t cap,
+                                          int64_t* __restrict__ out_edge,
+                                          int32_t* __restrict__ out_lat,
+                                          uint8_t* __restrict__ out_count,
+                                          double* __restrict__ out_xyz) {
+  const double z0 = tab[k];
+  sgi::QueryOut o;
+  if (!sgi::lat_query<MODE, sgi::Fast>(pre, in, z0, o)) {
+    const sgi::RegIn r = {{in(0), in(1), in(2), in(3), in(4), in(5)}};
+    sgi::query_exact<MODE>(r, z0, o);
+  }
+  const bool deg = o.count == sgi::kDegenerate;
+  const double nan = sgi::qnan();
+  out_edge[j] = edge;
+  out_lat[j] = k;
+  out_count[j] = o.count;
+  __stcs(out_xyz + 0 * cap + j, o.p0x);
+  __stcs(out_xyz + 1 * cap + j, o.p0y);
+  __stcs(out_xyz + 2 * cap + j, (!deg && o.count >= 1) ? z0 : nan);
+  __stcs(out_xyz + 3 * cap + j, o.p1x);
+  __stcs(out_xyz + 4 * cap + j, o.p1y);
+  __stcs(out_xyz + 5 * cap + j, (!deg && o.count == 2) ? z0 : nan);
+}
 
 template <int MODE>
-__global__ void __launch_bounds__(kTile)
+__global__ void __launch_bounds__(kThreads, 512 / kThreads)
 sgi_zonal_emit_kernel(const double* __restrict__ va, const double* __restrict__ vb, int64_t ne,
                       int64_t lde, const double* __restrict__ lat, int nlat, int64_t cap,
                       int64_t* __restrict__ out_edge, int32_t* __restrict__ out_lat,
                       uint8_t* __restrict__ out_count, double* __restrict__ out_xyz,
-                      const unsigned long long* __restrict__ cta_base) {
-  extern __shared__ __align__(16) double s_lat[];
-  __shared__ double s_xyz[kTile][6];
-  __shared__ sgi::EdgePre s_pre[kTile];
-  __shared__ int s_klo[kTile], s_off[kTile];
-  __shared__ int s_warp[kTile / 32];
+                      const int2* __restrict__ cand,
+                      const unsigned long long* __restrict__ tile_base) {
+  extern __shared__ __align__(16) double s_dyn[];
+  __shared__ unsigned long long s_warp[kThreads / 32];
   const int tid = threadIdx.x;
-  const double* tab = stage_lat(s_lat, lat, nlat);
-  int64_t lo, hi;
-  cta_range(ne, lo, hi);
-  int64_t base = (int64_t)cta_base[blockIdx.x];
-  EdgeX cur;
-  if (lo + tid < hi) load_edge(cur, va, vb, lde, lo + tid);
-  for (int64_t t0 = lo; t0 < hi && base < cap; t0 += kTile) {
-    const int64_t e = t0 + tid;
-    EdgeX nxt;
-    if (e + kTile < hi) load_edge(nxt, va, vb, lde, e + kTile);
-    int klo = 0, kcnt = 0;
-    if (e < hi) {
-      candidates(cur.x, tab, nlat, klo, kcnt);
-#pragma unroll
-      for (int c = 0; c < 6; ++c) s_xyz[tid][c] = cur.x[c];
-      if (kcnt > 0) {
-        const sgi::RegIn in = {{cur.x[0], cur.x[1], cur.x[2], cur.x[3], cur.x[4], cur.x[5]}};
-        s_pre[tid] = sgi::edge_pre<MODE>(in);
+  const size_t lat_words = nlat <= kLatSmem ? ((size_t)nlat + 1) / 2 * 2 : 0;
+  EmitSmem& S = *reinterpret_cast<EmitSmem*>(s_dyn + lat_words);
+  const double* tab = stage_lat(s_dyn, lat, nlat);
+  const int64_t ntiles = (ne + kEdges - 1) / kEdges;
+  int buf = 0;
+  if ((int64_t)blockIdx.x < ntiles) stage_tile(S.stage[0], blockIdx.x, ne, lde, va, vb, cand);
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, buf ^= 1) {
+    asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's copies of tile t
+    EmitStage& G = S.stage[buf];
+    EmitList& L = S.list[buf];
+    const int64_t base = (int64_t)tile_base[t];
+    const int l0 = 2 * tid;
+    const int64_t e0 = t * kEdges + l0;
+    const int2 c0 = e0 < ne ? G.cand[l0] : make_int2(0, 0);
+    const int2 c1 = e0 + 1 < ne ? G.cand[l0 + 1] : make_int2(0, 0);
+    // pairs (high 40 bits) and candidate flags (low 24 bits) of this thread's two edges
+    const unsigned long long pairs = (unsigned long long)(unsigned)c0.y + (unsigned)c1.y;
+    const unsigned flags = (c0.y > 0) + (c1.y > 0);
+    const unsigned long long mine = (pairs << 24) | flags;
+    unsigned long long tot;
+    const unsigned long long excl = block_scan(mine, s_warp, &tot) - mine;  // (barriers)
+    const int ncand = (int)(tot & 0xFFFFFF);
+    const int64_t npairs = (int64_t)(tot >> 24);
+    int slot = (int)(excl & 0xFFFFFF);
+    int64_t poff = (int64_t)(excl >> 24);
+    if (c0.y > 0) {
+      L.edge[slot] = l0; L.klo[slot] = c0.x; L.kcnt[slot] = c0.y; L.off[slot] = poff; ++slot;
+    }
+    poff += c0.y;
+    if (c1.y > 0) { L.edge[slot] = l0 + 1; L.klo[slot] = c1.x; L.kcnt[slot] = c1.y; L.off[slot] = poff; }
+    // the list is complete, every thread's tile-t data is visible, and every thread is done
+    // with tile t - gridDim.x, whose buffer the next tile's copies now overwrite
+    const bool dense = __syncthreads_or(c0.y > kFuseMax || c1.y > kFuseMax);
+    const int64_t tn = t + gridDim.x;
+    if (tn < ntiles) stage_tile(S.stage[buf ^ 1], tn, ne, lde, va, vb, cand);
+    const uint32_t gx = smem_u32(&G.x[0][0]);
+    if (!dense) {
+      for (int c = tid; c < ncand; c += kThreads) {     // head once, then its latitudes
+        const int le = L.edge[c];
+        const sgi::SmemIn in = {gx + (uint32_t)le * 8u, (uint32_t)(kEdges * 8)};
+        const sgi::EdgePre pre = sgi::edge_pre<MODE>(in);
+        const int kc = L.kcnt[c], k0 = L.klo[c];
+        const int64_t j0 = base + L.off[c];
+        for (int q = 0; q < kc && j0 + q < cap; ++q)
+          emit_pair<MODE>(pre, in, t * kEdges + le, k0 + q, tab, j0 + q, cap, out_edge, out_lat,
+                          out_count, out_xyz);
+      }
+    } else {
+      for (int64_t p = tid; p < npairs && base + p < cap; p += kThreads) {
+        int l = 0, h = ncand;                            // owner candidate: last off[l] <= p
+        while (h - l > 1) {
+          const int mid = (l + h) >> 1;
+          if (L.off[mid] <= p) l = mid; else h = mid;
+        }
+        const int le = L.edge[l];
+        const sgi::SmemIn in = {gx + (uint32_t)le * 8u, (uint32_t)(kEdges * 8)};
+        emit_pair<MODE>(sgi::edge_pre<MODE>(in), in, t * kEdges + le,
+                        L.klo[l] + (int)(p - L.off[l]), tab, base + p, cap, out_edge, out_lat,
+                        out_count, out_xyz);
       }
     }
-    s_klo[tid] = klo;
-    int total;
-    const int incl = block_scan(kcnt, s_warp, &total);
-    s_off[tid] = incl - kcnt;
-    __syncthreads();                                 // staging and offsets complete
-    for (int c = tid; c < total; c += kTile) {
-      const int64_t j = base + c;
-      if (j >= cap) break;
-      int l = 0, h = kTile;                          // owner edge: last s_off[t] <= c
-      while (h - l > 1) {
-        int mid = (l + h) >> 1;
-        if (s_off[mid] <= c) l = mid; else h = mid;
-      }
-      const int t = l;
-      const int k = s_klo[t] + (c - s_off[t]);
-      const double z0 = tab[k];
-      const SmemEdge in = {s_xyz[t]};
-      sgi::QueryOut o;
-      if (!sgi::lat_query<MODE, sgi::Fast>(s_pre[t], in, z0, o)) {
-        const sgi::RegIn r = {{in(0), in(1), in(2), in(3), in(4), in(5)}};
-        sgi::query_exact<MODE>(r, z0, o);
-      }
-      const bool deg = o.count == sgi::kDegenerate;
-      const double nan = sgi::qnan();
-      out_edge[j] = t0 + t;
-      out_lat[j] = k;
-      out_count[j] = o.count;
-      __stcs(out_xyz + 0 * cap + j, o.p0x);
-      __stcs(out_xyz + 1 * cap + j, o.p0y);
-      __stcs(out_xyz + 2 * cap + j, (!deg && o.count >= 1) ? z0 : nan);
-      __stcs(out_xyz + 3 * cap + j, o.p1x);
-      __stcs(out_xyz + 4 * cap + j, o.p1y);
-      __stcs(out_xyz + 5 * cap + j, (!deg && o.count == 2) ? z0 : nan);
-    }
-    base += total;
-    cur = nxt;
-    __syncthreads();                                 // smem of this tile is free
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 }  // namespace
@@ -282,7 +422,8 @@ extern "C" {
 
 size_t sgi_zonal_workspace_bytes(int64_t n_edges) {
   if (n_edges < 0) return 0;
-  return (size_t)kMaxCtas * sizeof(unsigned long long);
+  const int64_t ntiles = (n_edges + kEdges - 1) / kEdges;
+  return (size_t)n_edges * sizeof(int2) + (size_t)(ntiles + 1) * sizeof(unsigned long long);
 }
 
 sgi_status sgi_zonal_intersect(const double* va, const double* vb, int64_t n_edges, int64_t ld_e,
@@ -316,36 +457,28 @@ sgi_status sgi_zonal_intersect(const double* va, const double* vb, int64_t n_edg
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t lat_smem = n_lat <= kLatSmem ? (size_t)n_lat * sizeof(double) : 0;
-  const int64_t tiles = (n_edges + kTile - 1) / kTile;
-  unsigned long long* cta = (unsigned long long*)d_work;
-  const size_t emit_smem = kEmitSmem + lat_smem;
+  const size_t lat_smem_even = n_lat <= kLatSmem ? ((size_t)n_lat + 1) / 2 * 2 * sizeof(double) : 0;
+  const size_t emit_smem = lat_smem_even + sizeof(EmitSmem);
+  const int64_t ntiles = (n_edges + kEdges - 1) / kEdges;
+  int2* cand = (int2*)d_work;
+  unsigned long long* tile = (unsigned long long*)((char*)d_work + (size_t)n_edges * sizeof(int2));
+  // persistent grids: resident CTAs per SM x SMs, capped by the tile count
   auto grid_for = [&](auto kernel, size_t smem) {
     int occ = 1;
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(kEmitSmem + kLatSmem * sizeof(double)));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kTile, smem);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem);
     int64_t g = (int64_t)sms * (occ < 1 ? 1 : occ);
-    if (g > tiles) g = tiles;
-    if (g > kMaxCtas) g = kMaxCtas;
-    return (int)g;
+    return (int)(g < ntiles ? g : ntiles);
   };
-  // both passes use the same grid so each CTA walks the same edge range
-  int grid = 0;
-  switch (mode) {
-    case SGI_MODE_NAIVE: grid = grid_for(sgi_zonal_emit_kernel<sgi::MODE_NAIVE>, emit_smem); break;
-    case SGI_MODE_EFT: grid = grid_for(sgi_zonal_emit_kernel<sgi::MODE_EFT>, emit_smem); break;
-    case SGI_MODE_EFT_LITERAL: grid = grid_for(sgi_zonal_emit_kernel<sgi::MODE_EFT_LITERAL>, emit_smem); break;
-    case SGI_MODE_YAC: grid = grid_for(sgi_zonal_emit_kernel<sgi::MODE_YAC>, emit_smem); break;
-    case SGI_MODE_BASE: grid = grid_for(sgi_zonal_emit_kernel<sgi::MODE_BASE>, emit_smem); break;
-    default: grid = grid_for(sgi_zonal_emit_kernel<sgi::MODE_NAIVE_KAHAN>, emit_smem); break;
-  }
-  grid_for(sgi_zonal_count_kernel, lat_smem);
-  sgi_zonal_count_kernel<<<grid, kTile, lat_smem, st>>>(va, vb, n_edges, ld_e, lat_z0, n_lat, cta);
-  sgi_zonal_scan_kernel<<<1, 1024, 0, st>>>(cta, grid, d_total);
+  const int gf = grid_for(sgi_zonal_filter_kernel, lat_smem);
+  sgi_zonal_filter_kernel<<<gf, kThreads, lat_smem, st>>>(va, vb, n_edges, ld_e, lat_z0, n_lat,
+                                                          cand, tile);
+  sgi_zonal_scan_kernel<<<1, kScanThreads, 0, st>>>(tile, ntiles, d_total);
   if (cap > 0) {
     auto emit = [&](auto kernel) {
-      kernel<<<grid, kTile, emit_smem, st>>>(va, vb, n_edges, ld_e, lat_z0, n_lat, cap, out_edge,
-                                             out_lat, out_count, out_xyz, cta);
+      const int ge = grid_for(kernel, emit_smem);
+      kernel<<<ge, kThreads, emit_smem, st>>>(va, vb, n_edges, ld_e, lat_z0, n_lat, cap, out_edge,
+                                              out_lat, out_count, out_xyz, cand, tile);
     };
     switch (mode) {
       case SGI_MODE_NAIVE: emit(sgi_zonal_emit_kernel<sgi::MODE_NAIVE>); break;

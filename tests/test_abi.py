@@ -86,7 +86,9 @@ def test_zonal_validates_arguments(lib):
     assert lib.sgi_zonal_intersect(e.ctypes.data, e.ctypes.data, 8, 8, lat.ctypes.data, 4, 0,
                                    None, None, None, None, tot.ctypes.data, None, 0, 1,
                                    None) == sgi.SGI_E_INVALID          # no workspace
-    assert sgi.zonal_workspace_bytes(0) == 32768 and sgi.zonal_workspace_bytes(1 << 30) == 32768
+    assert sgi.zonal_workspace_bytes(0) == 8                       # the tile-sum terminator
+    assert sgi.zonal_workspace_bytes(1000) == 1000 * 8 + (2 + 1) * 8   # 512-edge tiles
+    assert sgi.zonal_workspace_bytes(-1) == 0
 
 
 def test_host_entry_validates_workspace(lib):

@@ -1,0 +1,98 @@
+"""Build and time launch-shape variants of the fused zonal pass (tools, not product).
+    python tools/zonal_variants.py build      # here
+    python tools/zonal_variants.py time       # on the GPU: C4 mesh x 1,800 latitudes
+Knobs: SGI_ZONAL_THREADS (tile = 2x edges), SGI_ZONAL_FUSE, SGI_ZONAL_EMIT_MINB."""
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+OUT = os.path.join(ROOT, "build", "zvariants")
+VARIANTS = {
+    "t256": {},
+    "t128": {"SGI_ZONAL_THREADS": 128},
+}
+OLD = {
+    "t256": {},
+    "t256_fuse4": {"SGI_ZONAL_FUSE": 4},
+    "t128_b4": {"SGI_ZONAL_THREADS": 128, "SGI_ZONAL_EMIT_MINB": 4},
+    "t512_b1": {"SGI_ZONAL_THREADS": 512, "SGI_ZONAL_EMIT_MINB": 1},
+}
+
+
+def build():
+    from paper_2510_09892_b200._build import NVCC_FLAGS
+    os.makedirs(OUT, exist_ok=True)
+    srcs = [os.path.join(ROOT, "paper_2510_09892_b200", "csrc", f) for f in ("sgi_capi.cu", "sgi_zonal.cu")]
+    for name, defs in VARIANTS.items():
+        d = [f"-D{k}={v}" for k, v in defs.items()]
+        lib = os.path.join(OUT, f"libsgi_{name}.so")
+        r = subprocess.run(["nvcc", *NVCC_FLAGS, *d, "-I", os.path.join(ROOT, "include"), "-o", lib,
+                            *srcs], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
+        print(name, "ok")
+
+
+def time_all(rounds=5, reps=10):
+    import torch
+    import sgi_inputs
+    va, vb = sgi_inputs.cubed_sphere_edges(1024)
+    lat = sgi_inputs.latitudes(1800)
+    dva, dvb = torch.from_numpy(va).cuda(), torch.from_numpy(vb).cuda()
+    dl = torch.from_numpy(lat).cuda()
+    ne = va.shape[1]
+    vp, i64 = ctypes.c_void_p, ctypes.c_int64
+    libs = {}
+    for name in VARIANTS:
+        L = ctypes.CDLL(os.path.join(OUT, f"libsgi_{name}.so"))
+        L.sgi_zonal_intersect.restype = ctypes.c_int
+        L.sgi_zonal_intersect.argtypes = [vp, vp, i64, i64, vp, ctypes.c_int32, i64, vp, vp, vp,
+                                          vp, vp, vp, ctypes.c_size_t, ctypes.c_int, vp]
+        L.sgi_zonal_workspace_bytes.restype = ctypes.c_size_t
+        L.sgi_zonal_workspace_bytes.argtypes = [i64]
+        libs[name] = L
+    cap = 6_100_000
+    outs = {"edge": torch.empty(cap, dtype=torch.int64, device="cuda"),
+            "lat": torch.empty(cap, dtype=torch.int32, device="cuda"),
+            "count": torch.empty(cap, dtype=torch.uint8, device="cuda"),
+            "xyz": torch.empty((2, 3, cap), dtype=torch.float64, device="cuda")}
+    total = torch.zeros(1, dtype=torch.int64, device="cuda")
+    st = torch.cuda.current_stream()
+    times = {n: [] for n in VARIANTS}
+    ref = None
+    same = {}
+    for r in range(rounds):
+        for name, L in libs.items():
+            work = torch.empty(L.sgi_zonal_workspace_bytes(ne), dtype=torch.uint8, device="cuda")
+            call = lambda: L.sgi_zonal_intersect(  # noqa: E731
+                dva.data_ptr(), dvb.data_ptr(), ne, ne, dl.data_ptr(), len(lat), cap,
+                outs["edge"].data_ptr(), outs["lat"].data_ptr(), outs["count"].data_ptr(),
+                outs["xyz"].data_ptr(), total.data_ptr(), work.data_ptr(), work.numel(), 1,
+                ctypes.c_void_p(st.cuda_stream))
+            for _ in range(2):
+                assert call() == 0
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                call()
+            e1.record()
+            torch.cuda.synchronize()
+            times[name].append(e0.elapsed_time(e1) / reps)
+            if r == 0:
+                m = int(total.item())
+                cur = (outs["edge"][:m].clone(), outs["xyz"][..., :m].clone())
+                if ref is None:
+                    ref = cur
+                same[name] = torch.equal(cur[0], ref[0]) and torch.equal(
+                    cur[1].view(torch.int64), ref[1].view(torch.int64))
+    for name in VARIANTS:
+        print(json.dumps({"variant": name, "ms_median": round(statistics.median(times[name]), 4),
+                          "ms_min": round(min(times[name]), 4), "same_as_first": same[name]}))
+
+
+if __name__ == "__main__":
+    build() if sys.argv[1] == "build" else time_all()
