@@ -64,6 +64,29 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// A bucket index over z in [-1, 1] turns each table search into one shared-memory lookup plus a
+// short binary search: bkt[b] = lower_bound(tab, -1 + 2b/kBuckets) for b = 0..kBuckets (the
+// boundaries are exact binary fractions).  For x in bucket b (computed up to one bucket of
+// rounding) the answer lies between the bounds of buckets b-1 and b+2; outside [-1, 1] the
+// bracket opens to the table's ends, so any strictly increasing table is handled.
+constexpr int kBuckets = 2048;
+
+__device__ __forceinline__ void build_buckets(int* bkt, const double* tab, int nlat) {
+  for (int b = threadIdx.x; b <= kBuckets; b += blockDim.x)
+    bkt[b] = lower_bound(tab, nlat, -1.0 + (double)b * (2.0 / kBuckets));
+  __syncthreads();
+}
+
+template <bool UPPER>   // false: first k with tab[k] >= x; true: first k with tab[k] > x
+__device__ __forceinline__ int bucket_search(const int* bkt, const double* tab, int nlat, double x) {
+  double f = __dmul_rn(__dadd_rn(x, 1.0), (double)(kBuckets / 2));
+  f = f < 0.0 ? 0.0 : (f > (double)(kBuckets - 1) ? (double)(kBuckets - 1) : f);
+  const int b = (int)f;
+  const int lo = b >= 1 ? bkt[b - 1] : 0;
+  const int hi = b + 2 <= kBuckets - 1 ? bkt[b + 2] : nlat;
+  return lo + (UPPER ? upper_bound(tab + lo, hi - lo, x) : lower_bound(tab + lo, hi - lo, x));
+}
+
 struct EdgeX {
   double x[6];
 };
@@ -77,9 +100,9 @@ __device__ __forceinline__ void load_edge(EdgeX& r, const double* __restrict__ v
 // Candidate latitudes [klo, klo + kcnt) of one edge (see the file comment).  The filter needs the
 // direction of n only to a few ulps: it takes the renormalised EFT normal's high parts (RN of the
 // exact n, so short arcs keep their accuracy) and evaluates heights with the device rsqrt (a few
-// ulps, deterministic) — errors ~1e-15, far below delta.  count and emit run this same code.
-__device__ __forceinline__ void candidates(const double* x, const double* tab, int nlat, int& klo,
-                                           int& kcnt) {
+// ulps, deterministic) — errors ~1e-15, far below delta.
+__device__ __forceinline__ void candidates(const double* x, const double* tab, const int* bkt,
+                                           int nlat, int& klo, int& kcnt) {
   klo = 0;
   kcnt = 0;
   const sgi::dd nxp = sgi::accu_dop(x[1], x[5], x[2], x[4]);
@@ -92,24 +115,20 @@ __device__ __forceinline__ void candidates(const double* x, const double* tab, i
   const double za = __dmul_rn(x[2], rsqrt(ra2)), zb = __dmul_rn(x[5], rsqrt(rb2));
   const double g1 = __dsub_rn(__dmul_rn(nx, x[1]), __dmul_rn(ny, x[0]));
   const double g2 = __dsub_rn(__dmul_rn(nx, x[4]), __dmul_rn(ny, x[3]));
-  const double s2 = __dadd_rn(__dmul_rn(nx, nx), __dmul_rn(ny, ny));
-  const double s3 = __dadd_rn(s2, __dmul_rn(nz, nz));
-  const double h = s3 > 0.0 ? __dmul_rn(__dsqrt_rn(s2), rsqrt(s3)) : 0.0;
   double zhi = fmax(za, zb), zlo = fmin(za, zb);
-  if (g1 > 0.0 && g2 < 0.0) zhi = fmax(zhi, h);
-  if (g1 < 0.0 && g2 > 0.0) zlo = fmin(zlo, -h);
+  const bool top_inside = g1 > 0.0 && g2 < 0.0, bottom_inside = g1 < 0.0 && g2 > 0.0;
+  if (top_inside || bottom_inside) {                 // the circle's extremum is on the arc
+    const double s2 = __dadd_rn(__dmul_rn(nx, nx), __dmul_rn(ny, ny));
+    const double s3 = __dadd_rn(s2, __dmul_rn(nz, nz));
+    const double h = s3 > 0.0 ? __dmul_rn(__dsqrt_rn(s2), rsqrt(s3)) : 0.0;
+    if (top_inside) zhi = fmax(zhi, h);
+    else zlo = fmin(zlo, -h);
+  }
   if (nx == 0.0 && ny == 0.0 && nz == 0.0) {
     kcnt = nlat;                                     // n = 0: degenerate at every latitude
   } else if (zhi == zhi && zlo == zlo) {             // NaN inputs: no candidates
-    klo = lower_bound(tab, nlat, __dsub_rn(zlo, kDelta));
-    // the upper end: most edges span 0-2 latitudes, so step forward a few entries before
-    // falling back to a binary search over the rest of the table
-    const double top = __dadd_rn(zhi, kDelta);
-    int khi = klo;
-#pragma unroll
-    for (int j = 0; j < 3; ++j) khi += (khi < nlat && tab[khi] <= top) ? 1 : 0;
-    if (khi < nlat && tab[khi] <= top) khi = khi + upper_bound(tab + khi, nlat - khi, top);
-    kcnt = khi - klo;
+    klo = bucket_search<false>(bkt, tab, nlat, __dsub_rn(zlo, kDelta));
+    kcnt = bucket_search<true>(bkt, tab, nlat, __dadd_rn(zhi, kDelta)) - klo;
   }
 }
 
@@ -160,7 +179,9 @@ sgi_zonal_filter_kernel(const double* __restrict__ va, const double* __restrict_
                         int2* __restrict__ cand, unsigned long long* __restrict__ tile_sum) {
   extern __shared__ __align__(16) double s_lat[];
   __shared__ unsigned long long s_red[kThreads / 32];
+  __shared__ int s_bkt[kBuckets + 1];
   const double* tab = stage_lat(s_lat, lat, nlat);
+  build_buckets(s_bkt, tab, nlat);
   const int64_t ntiles = (ne + kEdges - 1) / kEdges;
   int64_t t = blockIdx.x;
   EdgeX cur[2];
@@ -180,7 +201,7 @@ sgi_zonal_filter_kernel(const double* __restrict__ va, const double* __restrict_
     for (int j = 0; j < 2; ++j) {
       if (e0 + j < ne) {
         int klo, kcnt;
-        candidates(cur[j].x, tab, nlat, klo, kcnt);
+        candidates(cur[j].x, tab, s_bkt, nlat, klo, kcnt);
         cand[e0 + j] = make_int2(klo, kcnt);
         sum += (unsigned)kcnt;
       }
