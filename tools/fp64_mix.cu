@@ -18,7 +18,9 @@ __device__ __forceinline__ float hif(double x) { return __int_as_float(__double2
 // kind 2: ordered TwoSum per chain: FSETP, 4 FSEL, 3 DADD
 // kind 3: Knuth TwoSum per chain: 6 DADD
 // kind 4: single dependent DADD chain (latency)
-// kind 5: DFMA with three distinct sources
+// kind 5: DFMA with three distinct sources (one a loop constant)
+// kind 6: DADD of two live chains (both operands fresh registers, no reuse)
+// kind 7: DFMA of three live chains (all operands fresh registers)
 template <int KIND>
 __global__ void mix(double* out, long long* cyc, int iters, double a, double b) {
   double x[CH], y[CH];
@@ -58,9 +60,23 @@ __global__ void mix(double* out, long long* cyc, int iters, double a, double b) 
       }
     } else if (KIND == 4) {
       x[0] = __dadd_rn(x[0], a);
-    } else {
+    } else if (KIND == 5) {
 #pragma unroll
       for (int c = 0; c < CH; ++c) x[c] = __fma_rn(x[c], y[c], b);
+    } else if (KIND == 6) {
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const double t = __dadd_rn(x[c], y[c]);
+        y[c] = __dadd_rn(y[c], x[(c + 1) % CH]);
+        x[c] = t;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const double t = __fma_rn(x[c], y[c], x[(c + 3) % CH]);
+        y[c] = __fma_rn(y[c], x[(c + 1) % CH], y[(c + 2) % CH]);
+        x[c] = t;
+      }
     }
   }
   long long t1 = clock64();
@@ -115,5 +131,7 @@ int main() {
   for (int w : {8, 16, 32}) run<3>("knuth twosum (+dmul)", w * 32, 1, CH * 7, 0);
   run<4>("dadd dependent latency", 32, 1, 1, 0);
   for (int w : {16, 32}) run<5>("dfma 3 sources", w * 32, 1, CH, 0);
+  for (int w : {16, 32}) run<6>("dadd 2 live operands", w * 32, 1, 2 * CH, 0);
+  for (int w : {16, 32}) run<7>("dfma 3 live operands", w * 32, 1, 2 * CH, 0);
   return 0;
 }

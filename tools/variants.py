@@ -16,10 +16,10 @@ sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "build", "variants")
 
 VARIANTS = {
-    "base": {'SGI_DBG_CLOCK': 1},
-    "pair_t512": {'SGI_EFT_PAIR': 1, 'SGI_DBG_CLOCK': 1},
-    "nostore": {'SGI_DBG_NOSTORE': 1, 'SGI_DBG_CLOCK': 1},
-    "noload_nostore": {'SGI_DBG_NOLOAD': 1, 'SGI_DBG_NOSTORE': 1, 'SGI_DBG_CLOCK': 1},
+    "base": {},
+    "pair_t384": {'SGI_EFT_THREADS': 384},
+    "knuth": {'SGI_TS_KNUTH': 1},
+    "nopair": {'SGI_EFT_PAIR': 0},
 }
 
 
