@@ -165,6 +165,33 @@ def cpu_baseline_run(config: int, n: int, mode: str):
     return n / dt, cores, dt
 
 
+def accuracy_sample(a, b, z0, out, cnt, ref_out, ref_cnt, mode, ref_mode, m=20_000):
+    """The metric's "max ulp err" (rank 0, N = 1, next to the cpu_baseline leg): the GPU's own
+    outputs of this run for a deterministic sample of m queries against oracle (b) (exact
+    rationals, Eq.FINAL).  err_u = |P~ - P| / (u sqrt(1 - z0^2)); the paper's bound
+    is 3 (Eq.BOUND).  Both modes of the run are scored."""
+    import numpy as np
+    from oracle import exact
+    n = cnt.shape[0]
+    idx = np.linspace(0, n - 1, min(m, n)).astype(np.int64)
+    ti = __import__("torch").from_numpy(idx).to(a.device)
+    A, B, Z = (x.index_select(-1, ti).cpu().numpy() for x in (a, b, z0))
+    res = {}
+    for name, o, c in ((mode, out, cnt), (ref_mode, ref_out, ref_cnt)):
+        O, C = o.index_select(-1, ti).cpu().numpy(), c.index_select(0, ti).cpu().numpy()
+        worst, viol, mism = 0.0, 0, 0
+        for j in range(len(idx)):
+            r = exact.check_query(A[:, j], B[:, j], Z[j], int(C[j]),
+                                  [(O[0, 0, j], O[0, 1, j]), (O[1, 0, j], O[1, 1, j])])
+            mism += not r["count_match"]
+            for e in r["err_u"]:
+                worst = max(worst, e)
+                viol += e > 3.0
+        res[name] = {"max_err_u": worst, "over_bound": viol, "count_mismatch_vs_exact": mism}
+    return {"bound_u": 3.0, "sample": f"{len(idx)} evenly spaced queries of this run's batch",
+            "reference": "oracle (b): exact rationals + 420-bit sqrt", **res}
+
+
 def run_reference(args):
     """--impl reference: the oracle on the host cores, each step a bounded sample (2^22 arcs)
     of the same workload; rank 0 only."""
@@ -313,8 +340,15 @@ def main():
     ms_local = e0.elapsed_time(e1)
     t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
     hist = sgi.count_histogram(cnt)                    # outside the timed region
-    if distributed:                                    # MAX of time, SUM of counts (NCCL)
-        sdist.reduce_after_step(t, hist)
+    # K5 output statistics (outside the timed region): |P| - 1 and Pz == z0 on every stored point,
+    # and the deviation from the naive-FP64 kernel on the same arcs
+    ref_mode = "naive" if mode != "naive" else "eft"
+    ref_out = torch.empty_like(out)
+    ref_cnt = torch.empty_like(cnt)
+    sgi.intersect_arc_lat(a, b, z0, mode=ref_mode, out_xyz=ref_out, out_count=ref_cnt, stream=stream)
+    stats, counts = sgi.output_stats(out, cnt, z0, ref_xyz=ref_out, ref_count=ref_cnt, stream=stream)
+    if distributed:                                    # MAX of time and stats, SUM of counts (NCCL)
+        sdist.reduce_after_step(t, hist, stats, counts)
     ms = float(t.item())
     total_arcs = n * ws * args.steps
     value = total_arcs / (ms * 1e-3)
@@ -378,11 +412,14 @@ def main():
         del ha, hb, hz, hout, hcnt, work
 
     cpu = None
+    accuracy = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         v, cores, dt = cpu_baseline_run(cfg, n, mode)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"the full per-rank batch ({n} arcs of config {cfg}) once through oracle "
                          f"(a) with OpenMP over {cores} threads ({dt:.2f} s)"}
+        accuracy = accuracy_sample(a, b, z0, out, cnt, ref_out, ref_cnt, mode, ref_mode)
+    del ref_out, ref_cnt
 
     if rank == 0:
         h = hist.cpu().tolist()
@@ -401,6 +438,12 @@ def main():
             "clocks": clocks.summary(),
             "gpu_launches": args.steps,
             "hist": {"zero": h[0], "one": h[1], "two": h[2], "degenerate": h[3], "points": h[4]},
+            "max_ulp_err": accuracy,
+            "output_stats": {
+                "max_norm_dev_u": float(stats[0]), f"max_dev_from_{ref_mode}_u": float(stats[1]),
+                "pz_not_z0": int(counts[0]), f"count_mismatch_vs_{ref_mode}": int(counts[1]),
+                "what": "sgi_output_stats over every stored point of every rank (NCCL MAX/SUM): "
+                        "||P|-1|/u, Pz bit copy of z0, |P - P_ref|/u vs the other mode"},
             "points_per_s": h[4] / (ms_per_step * 1e-3),
         }
         print(json.dumps(line), flush=True)

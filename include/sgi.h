@@ -114,6 +114,21 @@ sgi_status sgi_zonal_intersect(const double* va, const double* vb, int64_t n_edg
                                size_t work_bytes, int mode, void* stream);
 size_t sgi_zonal_workspace_bytes(int64_t n_edges);
 
+/* Output statistics (the per-rank quantities the multi-GPU run reduces with NCCL).
+ * Over the stored points of out_xyz/out_count (device; layout as above, n queries, leading
+ * dimension ld): d_stats2[0] = max |(|P~|) - 1| / u (Eq.FINAL's points lie on the unit sphere,
+ * P:307-308; |P~|^2 evaluated in double-word arithmetic), d_counts2[0] += number of points whose
+ * z is not a bit copy of z0.  If ref_xyz/ref_count (another result for the same queries, e.g.
+ * SGI_MODE_NAIVE) are given: d_counts2[1] += queries whose counts differ, d_stats2[1] = max over
+ * the others' points of |P~ - P~ref| / u (the paper's distance).  Both buffers are
+ * device memory the caller zeroes; maxima accumulate (atomic max), counts add.  Asynchronous on
+ * `stream`.  Errors: SGI_E_INVALID for n < 0, ld < n, a null pointer with n > 0, or only one of
+ * ref_xyz / ref_count. */
+sgi_status sgi_output_stats(const double* out_xyz, const uint8_t* out_count, const double* z0,
+                            int64_t n, int64_t ld, const double* ref_xyz,
+                            const uint8_t* ref_count, double* d_stats2,
+                            unsigned long long* d_counts2, void* stream);
+
 /* Appendix-A instrumentation (Appendix A: "we recorded these results as
  * pairs of doubles (the leading term and compensation term)").  For each query i, every
  * intermediate of the mode's op sequence — computed with the IEEE intrinsics, i.e. the values

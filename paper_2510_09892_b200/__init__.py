@@ -10,6 +10,7 @@ Public API (same names as the C ABI):
     count_histogram(out_count, n=None, hist=None, stream=None)
     zonal_intersect(va, vb, lat_z0, mode="eft", cap=None, stream=None)
     intersect_trace(a, b, z0, mode="eft", n=None, stream=None)   (Appendix-A intermediates)
+    output_stats(out_xyz, out_count, z0, ref_xyz=None, ref_count=None)  (K5 invariants)
     host_workspace_bytes(chunk), abi_version(), status_str(code), last_error()
 Layout: a[3, ld], b[3, ld], z0[ld] float64; out_xyz[2, 3, ld] float64; out_count[ld] uint8.
 """
@@ -58,6 +59,8 @@ def _load():
                                           vp, vp, vp, ctypes.c_size_t, ctypes.c_int, vp]
         L.sgi_zonal_workspace_bytes.restype = ctypes.c_size_t
         L.sgi_zonal_workspace_bytes.argtypes = [i64]
+        L.sgi_output_stats.restype = ctypes.c_int
+        L.sgi_output_stats.argtypes = [vp, vp, vp, i64, i64, vp, vp, vp, vp, vp]
         L.sgi_intersect_trace.restype = ctypes.c_int
         L.sgi_intersect_trace.argtypes = [vp, vp, vp, i64, i64, vp, vp, ctypes.c_int, vp]
         L.sgi_trace_fields.restype = ctypes.c_int
@@ -134,6 +137,26 @@ def intersect_arc_lat(a, b, z0, mode="eft", out_xyz=None, out_count=None, n=None
                                        _stream_ptr(stream))
     _check(rc, "sgi_intersect_arc_lat")
     return out_xyz, out_count
+
+
+def output_stats(out_xyz, out_count, z0, ref_xyz=None, ref_count=None, n=None, stats=None,
+                 counts=None, stream=None):
+    """sgi_output_stats: (stats float64[2] = [max ||P|-1|/u, max |P - Pref|/u], counts int64[2] =
+    [points with Pz != z0, count mismatches vs ref]) as CUDA tensors (accumulated if given)."""
+    import torch
+    ld = z0.shape[0]
+    n = ld if n is None else n
+    dev = z0.device
+    if stats is None:
+        stats = torch.zeros(2, dtype=torch.float64, device=dev)
+    if counts is None:
+        counts = torch.zeros(2, dtype=torch.int64, device=dev)
+    rc = _load().sgi_output_stats(out_xyz.data_ptr(), out_count.data_ptr(), z0.data_ptr(), n, ld,
+                                  None if ref_xyz is None else ref_xyz.data_ptr(),
+                                  None if ref_count is None else ref_count.data_ptr(),
+                                  stats.data_ptr(), counts.data_ptr(), _stream_ptr(stream))
+    _check(rc, "sgi_output_stats")
+    return stats, counts
 
 
 def intersect_trace(a, b, z0, mode="eft", n=None, stream=None):

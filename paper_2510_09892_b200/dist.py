@@ -31,13 +31,22 @@ def shard_strong(rank: int, world: int, n_total: int) -> tuple[int, int]:
     return lo, hi - lo
 
 
-def reduce_after_step(elapsed_ms, hist):
-    """MAX of the per-rank step time and SUM of the count histograms (in place; returns both).
+def reduce_after_step(elapsed_ms, hist, stats=None, counts=None):
+    """MAX of the per-rank step time and SUM of the count histograms (in place; returns them);
+    optionally MAX of the output statistics and SUM of their violation counts
+    (sgi_output_stats: SURVEY §8(e) "NCCL reduction of counts and max-ulp statistics").
 
-    `elapsed_ms` is a float64 tensor of shape (1,), `hist` an int64 tensor of shape (5,), both on
-    the process group's device (CUDA for NCCL, CPU for gloo).  No-op without a process group."""
+    `elapsed_ms` is a float64 tensor of shape (1,), `hist` an int64 tensor of shape (5,),
+    `stats` float64 and `counts` int64 tensors, all on the process group's device (CUDA for
+    NCCL, CPU for gloo).  No-op without a process group."""
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized():
         dist.all_reduce(elapsed_ms, op=dist.ReduceOp.MAX)
         dist.all_reduce(hist, op=dist.ReduceOp.SUM)
-    return elapsed_ms, hist
+        if stats is not None:
+            dist.all_reduce(stats, op=dist.ReduceOp.MAX)
+        if counts is not None:
+            dist.all_reduce(counts, op=dist.ReduceOp.SUM)
+    if stats is None and counts is None:
+        return elapsed_ms, hist
+    return elapsed_ms, hist, stats, counts

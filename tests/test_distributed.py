@@ -37,8 +37,10 @@ def _worker(rank, world, port, n_per_rank, config, q):
     _, cnt = oracle.intersect(oracle.MODE_EFT, a, b, z0)
     hist = torch.from_numpy(_hist(cnt))
     t = torch.tensor([10.0 + r], dtype=torch.float64)
-    t, hist = sdist.reduce_after_step(t, hist)
-    q.put((r, float(t.item()), hist.numpy().tolist()))
+    stats = torch.tensor([0.5 + r, 2.0 - r], dtype=torch.float64)
+    counts = torch.tensor([r, 2 * r], dtype=torch.int64)
+    t, hist, stats, counts = sdist.reduce_after_step(t, hist, stats, counts)
+    q.put((r, float(t.item()), hist.numpy().tolist(), stats.tolist(), counts.tolist()))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -59,9 +61,10 @@ def test_gloo_world2_sharded_histogram(config):
     a, b, z0 = sgi_inputs.generate_host(config, world * n)
     _, cnt = oracle.intersect(oracle.MODE_EFT, a, b, z0)
     want = _hist(cnt).tolist()
-    for r, t, h in res:
+    for r, t, h, st, ct in res:
         assert t == 11.0                       # MAX over ranks
         assert h == want                       # SUM of shard histograms == global histogram
+        assert st == [1.5, 2.0] and ct == [1, 2]   # MAX of statistics, SUM of violation counts
 
 
 def test_shard_ranges():

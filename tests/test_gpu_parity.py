@@ -308,3 +308,36 @@ def test_histogram_matches_bincount():
     c = cnt.cpu().numpy()
     assert hist.tolist() == [int((c == 0).sum()), int((c == 1).sum()), int((c == 2).sum()),
                              int((c == 0xFF).sum()), int((c == 1).sum() + 2 * (c == 2).sum())]
+
+
+# ------------------------------------------------------------- K5 output statistics (§8(e))
+def test_output_stats_kernel():
+    """sgi_output_stats against numpy on C3 (ill-conditioned: naive and EFT differ a lot):
+    max ||P|-1|/u (x87 extended precision on the host), Pz == z0, count mismatches and the
+    max EFT-vs-naive distance."""
+    n = 150_000
+    a, b, z0 = sgi_inputs.generate_host(3, n)
+    da, db, dz = (torch.from_numpy(x).cuda() for x in (a, b, z0))
+    o1, c1 = sgi.intersect_arc_lat(da, db, dz, mode="eft")
+    o2, c2 = sgi.intersect_arc_lat(da, db, dz, mode="naive")
+    st, ct = sgi.output_stats(o1, c1, dz, ref_xyz=o2, ref_count=c2)
+    st0, ct0 = sgi.output_stats(o1, c1, dz)
+    torch.cuda.synchronize()
+    O1, C1, O2, C2 = o1.cpu().numpy(), c1.cpu().numpy(), o2.cpu().numpy(), c2.cpu().numpy()
+    U = 2.0 ** -53
+    dev, rdev = 0.0, 0.0
+    for k in range(2):
+        m = (C1 == 1) | (C1 == 2) if k == 0 else (C1 == 2)
+        p = O1[k][:, m].astype(np.longdouble)
+        nrm = (p[0] * p[0] + p[1] * p[1] + p[2] * p[2]) - 1
+        dev = max(dev, float(np.abs(nrm).max() / 2 / U))
+        assert np.array_equal(O1[k][2, m].view(np.int64), z0[m].view(np.int64))
+        same = m & (C1 == C2)
+        d = np.hypot(O1[k][0, same] - O2[k][0, same], O1[k][1, same] - O2[k][1, same]) / U
+        rdev = max(rdev, float(d.max()))
+    s = st.cpu().numpy()
+    assert abs(s[0] - dev) <= 0.02 + 1e-3 * dev, (s[0], dev)
+    assert 0 < s[0] <= 4.0                     # |P~| within a few u of 1 (SURVEY §8(c.4))
+    assert s[1] == pytest.approx(rdev, rel=1e-12)
+    assert ct.cpu().tolist() == [0, int((C1 != C2).sum())]
+    assert ct0.cpu().tolist() == [0, 0] and st0.cpu().numpy()[1] == 0
