@@ -50,7 +50,11 @@ def parse():
     p.add_argument("--mode", default="eft",
                    choices=["eft", "eft_literal", "naive", "yac", "base", "naive_kahan"])
     p.add_argument("--config", type=int, default=2, choices=[2, 3, 5, 6, 7])
-    p.add_argument("--n", type=int, default=1 << 24, help="arcs per rank")
+    p.add_argument("--n", type=int, default=1 << 24,
+                   help="arcs per rank (--scaling weak) or in total (--scaling strong)")
+    p.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                   help="weak: every rank owns n arcs (default, C2); strong: the n arcs are split "
+                        "across the ranks (C5's 2^30 arcs over 1/2/4/8 GPUs)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -308,7 +312,11 @@ def main():
     if distributed:
         dist.init_process_group("nccl", device_id=dev)
     n, cfg, mode = args.n, args.config, args.mode
-    offset, n = sdist.shard_weak(rank, ws, n)           # this rank's slice of the index space
+    if args.scaling == "weak":                          # this rank's slice of the index space
+        offset, n = sdist.shard_weak(rank, ws, n)
+    else:
+        offset, n = sdist.shard_strong(rank, ws, n)
+    n_total = n * ws if args.scaling == "weak" else args.n
 
     # inputs generated on this rank's device from the seed (HBM resident before timing)
     a = torch.empty((3, n), dtype=torch.float64, device=dev)
@@ -350,7 +358,7 @@ def main():
     if distributed:                                    # MAX of time and stats, SUM of counts (NCCL)
         sdist.reduce_after_step(t, hist, stats, counts)
     ms = float(t.item())
-    total_arcs = n * ws * args.steps
+    total_arcs = n_total * args.steps
     value = total_arcs / (ms * 1e-3)
     ms_per_step = ms / args.steps
     launch_s = ms_local * 1e-3 / args.steps             # one kernel launch per step
@@ -405,8 +413,8 @@ def main():
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_s = float(te.item()) * 1e-3 / args.e2e_steps
         link = pcie_concurrent_gbs(dev)
-        e2e = {"value": n * ws / e2e_s, "unit": UNIT,
-               "h2d_bytes_per_step": n * 56 * ws, "d2h_bytes_per_step": n * 49 * ws,
+        e2e = {"value": n_total / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": n_total * 56, "d2h_bytes_per_step": n_total * 49,
                "steps": args.e2e_steps, "path": "sgi_intersect_arc_lat_host (pinned host buffers)",
                "link_gbs_measured": link, "link_frac": (n * 105 / e2e_s / 1e9) / link}
         del ha, hb, hz, hout, hcnt, work
@@ -426,9 +434,9 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": CONFIG_DESC[cfg], "mode": mode, "arcs_per_rank": n,
-                       "global_arcs_per_step": n * ws, "seed": SEEDS[cfg],
+                       "global_arcs_per_step": n_total, "seed": SEEDS[cfg],
                        "parallelism": f"arc-index shards x{ws}",
                        "l2": f"inputs larger than L2 ({n * 56 / 1e9:.2f} GB in + "
                              f"{n * 49 / 1e9:.2f} GB out per rank vs 126 MB L2)"},
