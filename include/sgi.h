@@ -114,6 +114,18 @@ sgi_status sgi_zonal_intersect(const double* va, const double* vb, int64_t n_edg
                                size_t work_bytes, int mode, void* stream);
 size_t sgi_zonal_workspace_bytes(int64_t n_edges);
 
+/* Double-word points (reading R11 — an extension: the paper rounds each
+ * coordinate once).  As sgi_intersect_arc_lat in an EFT mode (out_xyz and out_count
+ * are bit-identical to it), plus out_lo[(slot*2 + c)*ld + i], c = 0,1 = x,y: a low part with
+ * P ~ out_xyz + out_lo, from the root's numerator before CompDot's final rounding (the CompDotC
+ * pair, Alg.1) and |n_xy|^2 as a pair (Alg.7):  lo = -((fma(hi, S2, X) + ((p - X) +
+ * sigma)) + hi s2) / S2.  z needs no low part (P_z = z0 exactly).  Unused slots: canonical NaN.
+ * mode must be SGI_MODE_EFT or SGI_MODE_EFT_LITERAL (else SGI_E_INVALID); other errors as for
+ * sgi_intersect_arc_lat.  Device pointers, one launch on `stream`; not tuned. */
+sgi_status sgi_intersect_arc_lat_dw(const double* a, const double* b, const double* z0, int64_t n,
+                                    int64_t ld, double* out_xyz, double* out_lo,
+                                    uint8_t* out_count, int mode, void* stream);
+
 /* Output statistics (the per-rank quantities the multi-GPU run reduces with NCCL).
  * Over the stored points of out_xyz/out_count (device; layout as above, n queries, leading
  * dimension ld): d_stats2[0] = max |(|P~|) - 1| / u (Eq.FINAL's points lie on the unit sphere,

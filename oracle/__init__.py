@@ -55,6 +55,11 @@ def lib():
         L.oracle_intersect_batch.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                                              ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+        L.oracle_intersect_dw_batch.restype = ctypes.c_int
+        L.oracle_intersect_dw_batch.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                                ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                                ctypes.c_int]
         L.oracle_trace.restype = ctypes.c_int
         L.oracle_trace.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                                    ctypes.c_double, ctypes.c_void_p]
@@ -84,6 +89,24 @@ def intersect(mode: int, a: np.ndarray, b: np.ndarray, z0: np.ndarray, n: int | 
     if rc != 0:
         raise ValueError("oracle_intersect_batch rejected its arguments")
     return out, cnt
+
+
+def intersect_dw(mode: int, a: np.ndarray, b: np.ndarray, z0: np.ndarray, nthreads: int = 1):
+    """Oracle (a) with double-word points (EFT modes): (out_xyz[2,3,n], out_lo[2,2,n], count[n]);
+    P ~ out_xyz + out_lo per x/y coordinate (reading R11)."""
+    a = np.ascontiguousarray(a, np.float64)
+    b = np.ascontiguousarray(b, np.float64)
+    z0 = np.ascontiguousarray(z0, np.float64)
+    ld = z0.shape[0]
+    out = np.empty((2, 3, ld), np.float64)
+    lo = np.empty((2, 2, ld), np.float64)
+    cnt = np.empty(ld, np.uint8)
+    rc = lib().oracle_intersect_dw_batch(mode, a.ctypes.data, b.ctypes.data, z0.ctypes.data, ld,
+                                         ld, out.ctypes.data, lo.ctypes.data, cnt.ctypes.data,
+                                         nthreads)
+    if rc != 0:
+        raise ValueError("oracle_intersect_dw_batch rejected its arguments")
+    return out, lo, cnt
 
 
 def trace(mode: int, x1, x2, z0: float) -> tuple[int, dict]:

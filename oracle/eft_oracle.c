@@ -283,7 +283,7 @@ static double canonical_nan(void) {
 
 /* One query: count in {0,1,2,0xFF} and the two slots (x,y) in arc order (reading R7). */
 static uint8_t intersect_one(int mode, const double x1[3], const double x2[3], double z0,
-                             double slot[2][2], accux_trace* tr) {
+                             double slot[2][2], accux_trace* tr, int* plus_first) {
   accux_trace t;
   double hx, hy, hz;
   if (mode == OR_MODE_NAIVE) {
@@ -310,6 +310,7 @@ static uint8_t intersect_one(int mode, const double x1[3], const double x2[3], d
   int inp = (A1 >= B1) && (A2 <= B2);
   int inm = (t.sh > 0.0) && (A1 >= -B1) && (A2 <= -B2);
   count = (uint8_t)(inp + inm);
+  if (plus_first) *plus_first = count == 2 ? g1 >= 0.0 : inp;
   if (count == 2) {
     const double* first = g1 >= 0.0 ? t.Pp : t.Pm;
     const double* second = g1 >= 0.0 ? t.Pm : t.Pp;
@@ -339,7 +340,7 @@ int oracle_intersect_batch(int mode, const double* a, const double* b, const dou
     double x1[3] = {a[i], a[ld + i], a[2 * ld + i]};
     double x2[3] = {b[i], b[ld + i], b[2 * ld + i]};
     double slot[2][2];
-    uint8_t c = intersect_one(mode, x1, x2, z0[i], slot, 0);
+    uint8_t c = intersect_one(mode, x1, x2, z0[i], slot, 0, 0);
     double nan = canonical_nan();
     for (int k = 0; k < 2; ++k) {
       int used = (c != OR_DEGENERATE) && (k < c);
@@ -352,12 +353,61 @@ int oracle_intersect_batch(int mode, const double* a, const double* b, const dou
   return 0;
 }
 
+/* Double-word points (reading R11): for each stored slot, the low part
+ * `lo` with P ~ hi + lo, hi the stored (rounded) coordinate.  From the numerator's CompDotC pair
+ * (p, sigma) (Alg.1) of the root in that slot, its CompDot X = RN(p + sigma), and
+ * the pair (S2, s2) of |n_xy|^2 (Alg.7):
+ *   t  = fma(hi, S2, X)          exact remainder of the rounded division
+ *   dl = (p - X) + sigma         the numerator's low part
+ *   r  = (t + dl) + hi * s2      N + hi D  (N = p + sigma, D = S2 + s2)
+ *   lo = -(r / S2)               since -N/D = hi - (N + hi D)/D
+ * Unused slots hold the canonical NaN in both planes.  EFT modes only. */
+static double dw_lo(double hi, const double num_pair[2], double X, double S2, double s2) {
+  double t = fma(hi, S2, X);
+  double dl = (num_pair[0] - X) + num_pair[1];
+  double r = (t + dl) + (hi * s2);
+  return -(r / S2);
+}
+
+int oracle_intersect_dw_batch(int mode, const double* a, const double* b, const double* z0,
+                              int64_t n, int64_t ld, double* out_xyz, double* out_lo,
+                              uint8_t* out_count, int nthreads) {
+  if ((mode != OR_MODE_EFT && mode != OR_MODE_EFT_LITERAL) || n < 0 || ld < n) return 1;
+  if (nthreads < 1) nthreads = 1;
+#pragma omp parallel for schedule(static) num_threads(nthreads)
+  for (int64_t i = 0; i < n; ++i) {
+    double x1[3] = {a[i], a[ld + i], a[2 * ld + i]};
+    double x2[3] = {b[i], b[ld + i], b[2 * ld + i]};
+    double slot[2][2];
+    accux_trace t;
+    int plus_first = 1;
+    uint8_t c = intersect_one(mode, x1, x2, z0[i], slot, &t, &plus_first);
+    double nan = canonical_nan();
+    for (int k = 0; k < 2; ++k) {
+      int used = (c != OR_DEGENERATE) && (k < c);
+      out_xyz[(k * 3 + 0) * ld + i] = slot[k][0];
+      out_xyz[(k * 3 + 1) * ld + i] = slot[k][1];
+      out_xyz[(k * 3 + 2) * ld + i] = used ? z0[i] : nan;
+      double lx = nan, ly = nan;
+      if (used) {
+        int plus = (k == 0) == plus_first;
+        lx = dw_lo(slot[k][0], plus ? t.Xpp : t.Xmp, plus ? t.Xp : t.Xm, t.S2, t.s2);
+        ly = dw_lo(slot[k][1], plus ? t.Ypp : t.Ymp, plus ? t.Yp : t.Ym, t.S2, t.s2);
+      }
+      out_lo[(k * 2 + 0) * ld + i] = lx;
+      out_lo[(k * 2 + 1) * ld + i] = ly;
+    }
+    out_count[i] = c;
+  }
+  return 0;
+}
+
 /* Every intermediate of one query (Appendix-A instrumentation).  Fills 38 doubles
  * in the field order of accux_trace and returns the count. */
 int oracle_trace(int mode, const double x1[3], const double x2[3], double z0, double* out30) {
   accux_trace t;
   double slot[2][2];
-  int c = intersect_one(mode, x1, x2, z0, slot, &t);
+  int c = intersect_one(mode, x1, x2, z0, slot, &t, 0);
   memcpy(out30, &t, sizeof(t));
   return c;
 }

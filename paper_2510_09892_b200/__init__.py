@@ -11,6 +11,7 @@ Public API (same names as the C ABI):
     zonal_intersect(va, vb, lat_z0, mode="eft", cap=None, stream=None)
     intersect_trace(a, b, z0, mode="eft", n=None, stream=None)   (Appendix-A intermediates)
     output_stats(out_xyz, out_count, z0, ref_xyz=None, ref_count=None)  (K5 invariants)
+    intersect_arc_lat_dw(a, b, z0, mode="eft")                   (double-word points)
     host_workspace_bytes(chunk), abi_version(), status_str(code), last_error()
 Layout: a[3, ld], b[3, ld], z0[ld] float64; out_xyz[2, 3, ld] float64; out_count[ld] uint8.
 """
@@ -59,6 +60,8 @@ def _load():
                                           vp, vp, vp, ctypes.c_size_t, ctypes.c_int, vp]
         L.sgi_zonal_workspace_bytes.restype = ctypes.c_size_t
         L.sgi_zonal_workspace_bytes.argtypes = [i64]
+        L.sgi_intersect_arc_lat_dw.restype = ctypes.c_int
+        L.sgi_intersect_arc_lat_dw.argtypes = [vp, vp, vp, i64, i64, vp, vp, vp, ctypes.c_int, vp]
         L.sgi_output_stats.restype = ctypes.c_int
         L.sgi_output_stats.argtypes = [vp, vp, vp, i64, i64, vp, vp, vp, vp, vp]
         L.sgi_intersect_trace.restype = ctypes.c_int
@@ -137,6 +140,25 @@ def intersect_arc_lat(a, b, z0, mode="eft", out_xyz=None, out_count=None, n=None
                                        _stream_ptr(stream))
     _check(rc, "sgi_intersect_arc_lat")
     return out_xyz, out_count
+
+
+def intersect_arc_lat_dw(a, b, z0, mode="eft", n=None, stream=None):
+    """Double-word points (sgi_intersect_arc_lat_dw): -> (out_xyz[2,3,ld], out_lo[2,2,ld],
+    out_count[ld]); P ~ out_xyz + out_lo for x and y."""
+    import torch
+    ld = z0.shape[0]
+    n = ld if n is None else n
+    _cuda_f64(a, (3, ld), "a")
+    _cuda_f64(b, (3, ld), "b")
+    _cuda_f64(z0, (ld,), "z0")
+    out = torch.empty((2, 3, ld), dtype=torch.float64, device=z0.device)
+    lo = torch.empty((2, 2, ld), dtype=torch.float64, device=z0.device)
+    cnt = torch.empty(ld, dtype=torch.uint8, device=z0.device)
+    rc = _load().sgi_intersect_arc_lat_dw(a.data_ptr(), b.data_ptr(), z0.data_ptr(), n, ld,
+                                          out.data_ptr(), lo.data_ptr(), cnt.data_ptr(),
+                                          _mode(mode), _stream_ptr(stream))
+    _check(rc, "sgi_intersect_arc_lat_dw")
+    return out, lo, cnt
 
 
 def output_stats(out_xyz, out_count, z0, ref_xyz=None, ref_count=None, n=None, stats=None,

@@ -29,7 +29,7 @@ def test_header_declares_the_boundary():
         "sgi_intersect_arc_lat", "sgi_intersect_arc_lat_host", "sgi_host_workspace_bytes",
         "sgi_count_histogram", "sgi_status_str", "sgi_last_error", "sgi_abi_version",
         "sgi_zonal_intersect", "sgi_zonal_workspace_bytes", "sgi_intersect_trace",
-        "sgi_trace_fields", "sgi_output_stats"])
+        "sgi_trace_fields", "sgi_output_stats", "sgi_intersect_arc_lat_dw"])
 
 
 def test_library_exports_every_declared_symbol(lib):

@@ -341,3 +341,28 @@ def test_output_stats_kernel():
     assert s[1] == pytest.approx(rdev, rel=1e-12)
     assert ct.cpu().tolist() == [0, int((C1 != C2).sum())]
     assert ct0.cpu().tolist() == [0, 0] and st0.cpu().numpy()[1] == 0
+
+
+# ------------------------------------------------------- double-word points (§8(f4), R11)
+@pytest.mark.parametrize("config,n", [(1, 10_000), (3, 30_000), (6, 17 * 1000), (7, 13 * 1000)])
+@pytest.mark.parametrize("mode,omode", [("eft", oracle.MODE_EFT),
+                                        ("eft_literal", oracle.MODE_EFT_LITERAL)])
+def test_double_word_parity(config, n, mode, omode):
+    a, b, z0 = sgi_inputs.generate_host(config, n)
+    da, db, dz = (torch.from_numpy(x).cuda() for x in (a, b, z0))
+    out, lo, cnt = sgi.intersect_arc_lat_dw(da, db, dz, mode=mode)
+    plain, pcnt = sgi.intersect_arc_lat(da, db, dz, mode=mode)
+    torch.cuda.synchronize()
+    ref, rlo, rcnt = oracle.intersect_dw(omode, a, b, z0, nthreads=NTHREADS)
+    assert np.array_equal(cnt.cpu().numpy(), rcnt)
+    assert same(out.cpu().numpy(), ref).all()
+    assert same(lo.cpu().numpy(), rlo).all()
+    assert same(plain.cpu().numpy(), out.cpu().numpy()).all()      # hi part = the plain result
+    assert np.array_equal(pcnt.cpu().numpy(), rcnt)
+
+
+def test_double_word_rejects_plain_modes():
+    z = torch.zeros(8, dtype=torch.float64, device="cuda")
+    v = torch.zeros((3, 8), dtype=torch.float64, device="cuda")
+    with pytest.raises(sgi.SGIError):
+        sgi.intersect_arc_lat_dw(v, v, z, mode="naive")
