@@ -132,14 +132,6 @@ __device__ __forceinline__ void candidates(const double* x, const double* tab, c
   }
 }
 
-__device__ __forceinline__ const double* stage_lat(double* s_lat, const double* lat, int nlat) {
-  if (nlat <= kLatSmem) {
-    for (int k = threadIdx.x; k < nlat; k += kThreads) s_lat[k] = lat[k];
-    __syncthreads();
-    return s_lat;
-  }
-  return lat;
-}
 
 // Block-wide inclusive scan of one 64-bit value per thread (kThreads threads); returns the
 // inclusive value and leaves the block total in *total.
@@ -170,9 +162,11 @@ __device__ __forceinline__ unsigned long long block_scan(unsigned long long v,
 }
 
 // Pass 1: candidate latitudes of every edge, cand[e] = (klo, kcnt), and each tile's sum.
-// Persistent CTAs stride over the tiles (the latitude table is staged once per CTA); thread
-// tid owns edges 2 tid and 2 tid + 1 of a tile, the next tile's loads issued before this one's
-// arithmetic.
+// Persistent CTAs stride over the tiles (the latitude table and its bucket index are staged
+// once per CTA); thread tid owns edges 2 tid and 2 tid + 1 of a tile, the next tile's loads in
+// flight while it works on this one.  SMEM: the latitude table fits in shared memory (the
+// searches then compile to LDS).
+template <bool SMEM>
 __global__ void __launch_bounds__(kThreads)
 sgi_zonal_filter_kernel(const double* __restrict__ va, const double* __restrict__ vb, int64_t ne,
                         int64_t lde, const double* __restrict__ lat, int nlat,
@@ -180,7 +174,11 @@ sgi_zonal_filter_kernel(const double* __restrict__ va, const double* __restrict_
   extern __shared__ __align__(16) double s_lat[];
   __shared__ unsigned long long s_red[kThreads / 32];
   __shared__ int s_bkt[kBuckets + 1];
-  const double* tab = stage_lat(s_lat, lat, nlat);
+  if (SMEM) {
+    for (int k = threadIdx.x; k < nlat; k += kThreads) s_lat[k] = lat[k];
+    __syncthreads();
+  }
+  const double* tab = SMEM ? s_lat : lat;
   build_buckets(s_bkt, tab, nlat);
   const int64_t ntiles = (ne + kEdges - 1) / kEdges;
   int64_t t = blockIdx.x;
@@ -361,7 +359,7 @@ __device__ __forceinline__ void emit_pair(const sgi::EdgePre& pre, const IN& in,
   __stcs(out_xyz + 5 * cap + j, (!deg && o.count == 2) ? z0 : nan);
 }
 
-template <int MODE>
+template <int MODE, bool SMEM>
 __global__ void __launch_bounds__(kThreads, 512 / kThreads)
 sgi_zonal_emit_kernel(const double* __restrict__ va, const double* __restrict__ vb, int64_t ne,
                       int64_t lde, const double* __restrict__ lat, int nlat, int64_t cap,
@@ -372,9 +370,13 @@ sgi_zonal_emit_kernel(const double* __restrict__ va, const double* __restrict__ 
   extern __shared__ __align__(16) double s_dyn[];
   __shared__ unsigned long long s_warp[kThreads / 32];
   const int tid = threadIdx.x;
-  const size_t lat_words = nlat <= kLatSmem ? ((size_t)nlat + 1) / 2 * 2 : 0;
+  const size_t lat_words = SMEM ? ((size_t)nlat + 1) / 2 * 2 : 0;
   EmitSmem& S = *reinterpret_cast<EmitSmem*>(s_dyn + lat_words);
-  const double* tab = stage_lat(s_dyn, lat, nlat);
+  if (SMEM) {
+    for (int k = threadIdx.x; k < nlat; k += kThreads) s_dyn[k] = lat[k];
+    __syncthreads();
+  }
+  const double* tab = SMEM ? s_dyn : lat;
   const int64_t ntiles = (ne + kEdges - 1) / kEdges;
   int buf = 0;
   if ((int64_t)blockIdx.x < ntiles) stage_tile(S.stage[0], blockIdx.x, ne, lde, va, vb, cand);
@@ -491,9 +493,17 @@ sgi_status sgi_zonal_intersect(const double* va, const double* vb, int64_t n_edg
     int64_t g = (int64_t)sms * (occ < 1 ? 1 : occ);
     return (int)(g < ntiles ? g : ntiles);
   };
-  const int gf = grid_for(sgi_zonal_filter_kernel, lat_smem);
-  sgi_zonal_filter_kernel<<<gf, kThreads, lat_smem, st>>>(va, vb, n_edges, ld_e, lat_z0, n_lat,
-                                                          cand, tile);
+  const bool smem_tab = n_lat <= kLatSmem;
+  const size_t filter_smem = lat_smem;
+  if (smem_tab) {
+    const int gf = grid_for(sgi_zonal_filter_kernel<true>, filter_smem);
+    sgi_zonal_filter_kernel<true><<<gf, kThreads, filter_smem, st>>>(va, vb, n_edges, ld_e, lat_z0,
+                                                                     n_lat, cand, tile);
+  } else {
+    const int gf = grid_for(sgi_zonal_filter_kernel<false>, filter_smem);
+    sgi_zonal_filter_kernel<false><<<gf, kThreads, filter_smem, st>>>(va, vb, n_edges, ld_e, lat_z0,
+                                                                      n_lat, cand, tile);
+  }
   sgi_zonal_scan_kernel<<<1, kScanThreads, 0, st>>>(tile, ntiles, d_total);
   if (cap > 0) {
     auto emit = [&](auto kernel) {
@@ -501,14 +511,16 @@ sgi_status sgi_zonal_intersect(const double* va, const double* vb, int64_t n_edg
       kernel<<<ge, kThreads, emit_smem, st>>>(va, vb, n_edges, ld_e, lat_z0, n_lat, cap, out_edge,
                                               out_lat, out_count, out_xyz, cand, tile);
     };
+#define SGI_EMIT(M) (smem_tab ? emit(sgi_zonal_emit_kernel<M, true>) : emit(sgi_zonal_emit_kernel<M, false>))
     switch (mode) {
-      case SGI_MODE_NAIVE: emit(sgi_zonal_emit_kernel<sgi::MODE_NAIVE>); break;
-      case SGI_MODE_EFT: emit(sgi_zonal_emit_kernel<sgi::MODE_EFT>); break;
-      case SGI_MODE_EFT_LITERAL: emit(sgi_zonal_emit_kernel<sgi::MODE_EFT_LITERAL>); break;
-      case SGI_MODE_YAC: emit(sgi_zonal_emit_kernel<sgi::MODE_YAC>); break;
-      case SGI_MODE_BASE: emit(sgi_zonal_emit_kernel<sgi::MODE_BASE>); break;
-      default: emit(sgi_zonal_emit_kernel<sgi::MODE_NAIVE_KAHAN>); break;
+      case SGI_MODE_NAIVE: SGI_EMIT(sgi::MODE_NAIVE); break;
+      case SGI_MODE_EFT: SGI_EMIT(sgi::MODE_EFT); break;
+      case SGI_MODE_EFT_LITERAL: SGI_EMIT(sgi::MODE_EFT_LITERAL); break;
+      case SGI_MODE_YAC: SGI_EMIT(sgi::MODE_YAC); break;
+      case SGI_MODE_BASE: SGI_EMIT(sgi::MODE_BASE); break;
+      default: SGI_EMIT(sgi::MODE_NAIVE_KAHAN); break;
     }
+#undef SGI_EMIT
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) {
