@@ -17,9 +17,7 @@ OUT = os.path.join(ROOT, "build", "variants")
 
 VARIANTS = {
     "base": {},
-    "pair_t384": {'SGI_EFT_THREADS': 384},
-    "knuth": {'SGI_TS_KNUTH': 1},
-    "nopair": {'SGI_EFT_PAIR': 0},
+    "probe": {'SGI_DBG_CLOCK': 1},
 }
 
 
@@ -88,6 +86,11 @@ def time_all(n, rounds=7, reps=20, config=2):
                 torch.cuda.synchronize()
                 clocks.append(clock())
                 times[(name, mode)].append(e0.elapsed_time(e1) / reps)
+                if hasattr(libs[name], "sgi_dbg_fallbacks") and r == 0:
+                    libs[name].sgi_dbg_fallbacks.restype = ctypes.c_ulonglong
+                    fb = libs[name].sgi_dbg_fallbacks()
+                    print(json.dumps({"variant": name, "config": config,
+                                      "exact_recomputations_per_launch": fb / (reps + 3)}))
                 if hasattr(libs[name], "sgi_dbg_clock"):
                     buf = (ctypes.c_longlong * 2)()
                     libs[name].sgi_dbg_clock(buf)
