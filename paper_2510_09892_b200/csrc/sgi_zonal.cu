@@ -79,8 +79,10 @@ __device__ __forceinline__ void build_buckets(int* bkt, const double* tab, int n
 
 template <bool UPPER>   // false: first k with tab[k] >= x; true: first k with tab[k] > x
 __device__ __forceinline__ int bucket_search(const int* bkt, const double* tab, int nlat, double x) {
-  double f = __dmul_rn(__dadd_rn(x, 1.0), (double)(kBuckets / 2));
-  f = f < 0.0 ? 0.0 : (f > (double)(kBuckets - 1) ? (double)(kBuckets - 1) : f);
+  // the bucket only has to be right to within one (the bracket spans b-1 .. b+2): float32 is
+  // far more than enough (NaN never reaches here: the caller screens it)
+  const float f = fminf(fmaxf(__fmul_rn(__fadd_rn((float)x, 1.0f), (float)(kBuckets / 2)), 0.0f),
+                        (float)(kBuckets - 1));
   const int b = (int)f;
   const int lo = b >= 1 ? bkt[b - 1] : 0;
   const int hi = b + 2 <= kBuckets - 1 ? bkt[b + 2] : nlat;
@@ -95,6 +97,18 @@ __device__ __forceinline__ void load_edge(EdgeX& r, const double* __restrict__ v
                                           const double* __restrict__ vb, int64_t lde, int64_t e) {
   r.x[0] = __ldg(va + e); r.x[1] = __ldg(va + lde + e); r.x[2] = __ldg(va + 2 * lde + e);
   r.x[3] = __ldg(vb + e); r.x[4] = __ldg(vb + lde + e); r.x[5] = __ldg(vb + 2 * lde + e);
+}
+
+// 1/sqrt(x) for a normal positive x: the MUFU seed and two Newton steps (relative error a few
+// ulps) — the filter's heights only need to be far inside delta = 2^-40, and this avoids the
+// special-case branches of the library rsqrt.
+__device__ __forceinline__ double fast_rsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = __dmul_rn(0.5, x);
+  y = __fma_rn(y, __fma_rn(-h, __dmul_rn(y, y), 0.5), y);
+  y = __fma_rn(y, __fma_rn(-h, __dmul_rn(y, y), 0.5), y);
+  return y;
 }
 
 // Candidate latitudes [klo, klo + kcnt) of one edge (see the file comment).  The filter needs the
@@ -112,7 +126,7 @@ __device__ __forceinline__ void candidates(const double* x, const double* tab, c
   const double nz = __dadd_rn(nzp.hi, nzp.lo);
   const double ra2 = __dadd_rn(__dadd_rn(__dmul_rn(x[0], x[0]), __dmul_rn(x[1], x[1])), __dmul_rn(x[2], x[2]));
   const double rb2 = __dadd_rn(__dadd_rn(__dmul_rn(x[3], x[3]), __dmul_rn(x[4], x[4])), __dmul_rn(x[5], x[5]));
-  const double za = __dmul_rn(x[2], rsqrt(ra2)), zb = __dmul_rn(x[5], rsqrt(rb2));
+  const double za = __dmul_rn(x[2], fast_rsqrt(ra2)), zb = __dmul_rn(x[5], fast_rsqrt(rb2));
   const double g1 = __dsub_rn(__dmul_rn(nx, x[1]), __dmul_rn(ny, x[0]));
   const double g2 = __dsub_rn(__dmul_rn(nx, x[4]), __dmul_rn(ny, x[3]));
   double zhi = fmax(za, zb), zlo = fmin(za, zb);
@@ -120,7 +134,7 @@ __device__ __forceinline__ void candidates(const double* x, const double* tab, c
   if (top_inside || bottom_inside) {                 // the circle's extremum is on the arc
     const double s2 = __dadd_rn(__dmul_rn(nx, nx), __dmul_rn(ny, ny));
     const double s3 = __dadd_rn(s2, __dmul_rn(nz, nz));
-    const double h = s3 > 0.0 ? __dmul_rn(__dsqrt_rn(s2), rsqrt(s3)) : 0.0;
+    const double h = s2 > 0.0 ? __dmul_rn(__dmul_rn(s2, fast_rsqrt(s2)), fast_rsqrt(s3)) : 0.0;
     if (top_inside) zhi = fmax(zhi, h);
     else zlo = fmin(zlo, -h);
   }

@@ -15,12 +15,7 @@ OUT = os.path.join(ROOT, "build", "zvariants")
 VARIANTS = {
     "t256": {},
     "t128": {"SGI_ZONAL_THREADS": 128},
-}
-OLD = {
-    "t256": {},
-    "t256_fuse4": {"SGI_ZONAL_FUSE": 4},
-    "t128_b4": {"SGI_ZONAL_THREADS": 128, "SGI_ZONAL_EMIT_MINB": 4},
-    "t512_b1": {"SGI_ZONAL_THREADS": 512, "SGI_ZONAL_EMIT_MINB": 1},
+    "t64": {"SGI_ZONAL_THREADS": 64},
 }
 
 
