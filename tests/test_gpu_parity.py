@@ -366,3 +366,26 @@ def test_double_word_rejects_plain_modes():
     v = torch.zeros((3, 8), dtype=torch.float64, device="cuda")
     with pytest.raises(sgi.SGIError):
         sgi.intersect_arc_lat_dw(v, v, z, mode="naive")
+
+
+@pytest.mark.parametrize("shift_in,shift_out", [(0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("mode,omode", [("eft", oracle.MODE_EFT), ("naive", oracle.MODE_NAIVE)])
+def test_alignment_paths(shift_in, shift_out, mode, omode):
+    """8-B (not 16-B) aligned inputs take the LDG kernel, 8-B aligned outputs the
+    one-query-per-thread TMA kernel; every path gives the oracle's results."""
+    n = 70_001
+    a, b, z0 = sgi_inputs.generate_host(5, n)
+    def shifted(x, k):
+        flat = torch.empty(x.size + k, dtype=torch.float64, device="cuda")
+        v = flat[k:].view(x.shape)
+        v.copy_(torch.from_numpy(x))
+        return v
+    da, db, dz = shifted(a, shift_in), shifted(b, shift_in), shifted(z0, shift_in)
+    ob = torch.empty(6 * n + shift_out, dtype=torch.float64, device="cuda")
+    out = ob[shift_out:].view(2, 3, n)
+    cb = torch.empty(n + shift_out, dtype=torch.uint8, device="cuda")
+    cnt = cb[shift_out:]
+    sgi.intersect_arc_lat(da, db, dz, mode=mode, out_xyz=out, out_count=cnt)
+    torch.cuda.synchronize()
+    ref, rcnt = oracle.intersect(omode, a, b, z0, nthreads=NTHREADS)
+    assert_parity(out.cpu().numpy(), cnt.cpu().numpy(), ref, rcnt)
