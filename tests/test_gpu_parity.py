@@ -368,12 +368,13 @@ def test_double_word_rejects_plain_modes():
         sgi.intersect_arc_lat_dw(v, v, z, mode="naive")
 
 
-@pytest.mark.parametrize("shift_in,shift_out", [(0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("n", [70_001, 600_001])
+@pytest.mark.parametrize("shift_in,shift_out", [(0, 0), (0, 1), (1, 0), (1, 1)])
 @pytest.mark.parametrize("mode,omode", [("eft", oracle.MODE_EFT), ("naive", oracle.MODE_NAIVE)])
-def test_alignment_paths(shift_in, shift_out, mode, omode):
-    """8-B (not 16-B) aligned inputs take the LDG kernel, 8-B aligned outputs the
-    one-query-per-thread TMA kernel; every path gives the oracle's results."""
-    n = 70_001
+def test_alignment_paths(n, shift_in, shift_out, mode, omode):
+    """Small batches and 8-B (not 16-B) aligned inputs take the LDG kernel; large aligned
+    batches the TMA kernel, two-query (EFT, 16-B aligned outputs) or one-query (8-B aligned
+    outputs); every path gives the oracle's results."""
     a, b, z0 = sgi_inputs.generate_host(5, n)
     def shifted(x, k):
         flat = torch.empty(x.size + k, dtype=torch.float64, device="cuda")

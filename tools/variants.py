@@ -17,7 +17,7 @@ OUT = os.path.join(ROOT, "build", "variants")
 
 VARIANTS = {
     "base": {},
-    "probe": {'SGI_DBG_CLOCK': 1},
+    "ldg": {'SGI_USE_TMA': 0},
 }
 
 
