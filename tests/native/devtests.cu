@@ -9,6 +9,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "../../paper_2510_09892_b200/csrc/sgi_eft.cuh"
+#include "../../paper_2510_09892_b200/csrc/sgi_query.cuh"
 
 __device__ __forceinline__ uint64_t mix(uint64_t x) {
   x ^= x >> 33; x *= 0xff51afd7ed558ccdull; x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ull; x ^= x >> 33;
@@ -103,5 +104,60 @@ extern "C" __global__ void devtest_kernel(uint64_t seed, int64_t n, unsigned lon
 extern "C" int sgi_devtest(uint64_t seed, int64_t n, unsigned long long* d_out) {
   cudaMemset(d_out, 0, 10 * sizeof(unsigned long long));
   devtest_kernel<<<148 * 8, 256>>>(seed, n, d_out);
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : 1;
+}
+
+// ------------------------------------------------------------------------------------------
+// The device primitives one by one, in the op numbering of oracle_prim_batch (oracle (a)), so a
+// test can compare each against the CPU oracle bit for bit on the same rows.  SumOfSquares starts
+// from its first TwoProd as the production code does (reading A12: the first SumNonNeg with (0,0)
+// is an exact identity); CompDotC/CompDot are the CompDotC step of sgi_eft.cuh in a loop;
+// AccSqrt runs the Exact policy, or the Fast policy (then out[2i+1] is NaN where its guard
+// failed, i.e. where the production code would recompute).
+__global__ void devprim_kernel(int op, int k, const double* in, int width, int64_t n,
+                               double* out, int fast) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double* r = in + i * width;
+    sgi::dd p = {0.0, 0.0};
+    switch (op) {
+      case 0: p = sgi::two_sum(r[0], r[1]); break;
+      case 1: p = sgi::fast_two_sum(r[0], r[1]); break;
+      case 2: p = sgi::two_prod(r[0], r[1]); break;
+      case 3: p.hi = sgi::kahan_dop(r[0], r[1], r[2], r[3]); break;
+      case 4: p = sgi::accu_dop(r[0], r[3], r[1], r[2]); break;   // oracle order: a*d - b*c
+      case 5: p = sgi::sum_non_neg(sgi::dd{r[0], r[1]}, sgi::dd{r[2], r[3]}); break;
+      case 6: case 7: {
+        sgi::dd S = sgi::two_prod(r[0], r[0]);
+        for (int j = 1; j < k; ++j) S = sgi::sum_non_neg(S, sgi::two_prod(r[j], r[j]));
+        if (op == 6) { p = S; break; }
+        sgi::dd R = sgi::two_prod(r[0], r[k]);
+        for (int j = 1; j < k; ++j) sgi::cdc_step(R.hi, R.lo, r[j], r[k + j]);
+        p = sgi::fast_two_sum(S.hi, sgi::fma(2.0, sgi::add(R.hi, R.lo), S.lo));
+      } break;
+      case 8: {
+        bool ok_root = true, ok_div = true;
+        if (fast) {
+          p = sgi::acc_sqrt<sgi::Fast>(r[0], r[1], ok_root, ok_div);
+          if (!(ok_root && ok_div)) p.lo = sgi::qnan();
+        } else {
+          p = sgi::acc_sqrt<sgi::Exact>(r[0], r[1], ok_root, ok_div);
+        }
+      } break;
+      case 9: case 10: {
+        sgi::dd P = sgi::two_prod(r[0], r[k]);
+        for (int j = 1; j < k; ++j) sgi::cdc_step(P.hi, P.lo, r[j], r[k + j]);
+        p = op == 9 ? P : sgi::dd{sgi::add(P.hi, P.lo), 0.0};
+      } break;
+      default: break;
+    }
+    out[2 * i] = p.hi;
+    out[2 * i + 1] = p.lo;
+  }
+}
+
+extern "C" int sgi_devprim(int op, int k, const double* d_in, int width, int64_t n, double* d_out,
+                           int fast) {
+  devprim_kernel<<<148 * 4, 256>>>(op, k, d_in, width, n, d_out, fast);
   return cudaDeviceSynchronize() == cudaSuccess ? 0 : 1;
 }

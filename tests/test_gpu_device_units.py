@@ -30,3 +30,63 @@ def test_primitives_bitwise_on_device(seed):
     assert c[9] == 0, f"is_zero/is_pos/is_neg/is_nonneg != double comparisons: {c}"
     # the guards do fire on the tiny numerators / radicands the test feeds on purpose
     assert c[4] > 0 and c[6] > 0
+
+
+# ------------------------------------------ device primitives vs oracle (a), op by op
+import numpy as np  # noqa: E402
+
+import oracle  # noqa: E402
+from helpers import random_doubles  # noqa: E402
+
+PRIM_ROWS = {            # name: (width, k, exponent range of the entries)
+    "two_sum": (2, 0, (-200, 200)), "fast_two_sum": (2, 0, (-200, 200)),
+    "two_prod": (2, 0, (-200, 200)), "kahan_dop": (4, 0, (-100, 100)),
+    "accu_dop": (4, 0, (-100, 100)), "sum_non_neg": (4, 0, (-100, 100)),
+    "sum_of_squares": (3, 3, (-60, 60)), "sum_of_squares_c": (6, 3, (-60, 60)),
+    "acc_sqrt": (2, 0, (-300, 300)), "comp_dot_c": (12, 6, (-60, 60)),
+    "comp_dot": (12, 6, (-60, 60)),
+}
+
+
+def _rows(name, n, rng):
+    width, k, (lo, hi) = PRIM_ROWS[name]
+    r = random_doubles(rng, n * width, lo, hi).reshape(n, width)
+    if name == "fast_two_sum":                     # its precondition: |a| >= |b|
+        big = np.maximum(np.abs(r[:, 0]), np.abs(r[:, 1]))
+        small = np.minimum(np.abs(r[:, 0]), np.abs(r[:, 1]))
+        r[:, 0] = big * np.sign(r[:, 0]); r[:, 1] = small * np.sign(r[:, 1])
+    if name in ("accu_dop", "kahan_dop"):          # a*b close to c*d for a third of the rows
+        m = rng.random(n) < 1 / 3
+        r[m, 3] = r[m, 0] * r[m, 1] / r[m, 2] * (1 + rng.integers(-4, 5, m.sum()) * 2.0 ** -52)
+    if name == "sum_non_neg":                      # two non-negative pairs (hi, lo), |lo| <= u|hi|
+        r[:, 0] = np.abs(r[:, 0]); r[:, 2] = np.abs(r[:, 2])
+        r[:, 1] = r[:, 0] * rng.uniform(-1, 1, n) * 2.0 ** -54
+        r[:, 3] = r[:, 2] * rng.uniform(-1, 1, n) * 2.0 ** -54
+    if name == "sum_of_squares_c":                 # (x, e) with |e| <= u |x|
+        r[:, 3:] = r[:, :3] * rng.uniform(-1, 1, (n, 3)) * 2.0 ** -53
+    if name == "acc_sqrt":                         # (H, h) with |h| <= u|H|, some H <= 0
+        r[:, 1] = r[:, 0] * rng.uniform(-1, 1, n) * 2.0 ** -53
+        r[:, 0] = np.where(rng.random(n) < 0.9, np.abs(r[:, 0]), r[:, 0])
+        r[: n // 50, 0] = 0.0
+    return np.ascontiguousarray(r), k
+
+
+@pytest.mark.parametrize("name", list(PRIM_ROWS))
+def test_device_primitives_equal_oracle(name):
+    lib = ctypes.CDLL(build_devtests())
+    lib.sgi_devprim.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
+                                ctypes.c_int64, ctypes.c_void_p, ctypes.c_int]
+    rng = np.random.default_rng(hash(name) % 2**32)
+    n = 200_000
+    rows, k = _rows(name, n, rng)
+    ref = oracle.prim(name, rows, k)
+    din = torch.from_numpy(rows).cuda()
+    for fast in ((0, 1) if name == "acc_sqrt" else (0,)):
+        dout = torch.empty((n, 2), dtype=torch.float64, device="cuda")
+        assert lib.sgi_devprim(oracle.PRIM[name], k, ctypes.c_void_p(din.data_ptr()), rows.shape[1],
+                               n, ctypes.c_void_p(dout.data_ptr()), fast) == 0
+        got = dout.cpu().numpy()
+        keep = ~np.isnan(got[:, 1]) if fast else np.ones(n, bool)
+        assert keep.mean() > 0.97
+        same = (got[keep] == ref[keep]) | (np.isnan(got[keep]) & np.isnan(ref[keep]))
+        assert same.all(), f"{name} fast={fast}: {int((~same).sum())} values differ"
