@@ -8,6 +8,10 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_2510_09892_b200 as sgi  # noqa: E402
+if len(sys.argv) > 1:                       # time an alternative build of libsgi.so
+    import paper_2510_09892_b200._build as _b
+    _b.LIB_PATH = sys.argv[1]
+    sgi.LIB_PATH = sys.argv[1]
 import sgi_inputs  # noqa: E402
 
 n = 1 << 24
