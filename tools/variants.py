@@ -17,9 +17,7 @@ OUT = os.path.join(ROOT, "build", "variants")
 
 VARIANTS = {
     "base": {},
-    "t256x2": {'SGI_EFT_THREADS': 256, 'SGI_EFT_MINB': 2},
-    "t256x2_s4": {'SGI_EFT_THREADS': 256, 'SGI_EFT_MINB': 2, 'SGI_EFT_STAGES': 4},
-    "t512_s2": {'SGI_EFT_STAGES': 2},
+    "tma_store": {'SGI_EFT_TMA_STORE': 1},
 }
 
 
