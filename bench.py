@@ -166,7 +166,23 @@ def cpu_baseline_run(config: int, n: int, mode: str):
     t0 = time.perf_counter()
     oracle.intersect(m, a, b, z0, nthreads=cores)
     dt = time.perf_counter() - t0
-    return n / dt, cores, dt
+    # one core on a bounded prefix (1 thread, then all host cores)
+    n1 = min(n, 1 << 21)
+    t1 = time.perf_counter()
+    oracle.intersect(m, a[:, :n1], b[:, :n1], z0[:n1], nthreads=1)
+    single = n1 / (time.perf_counter() - t1)
+    return n / dt, cores, dt, single
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def accuracy_sample(a, b, z0, out, cnt, ref_out, ref_cnt, mode, ref_mode, m=20_000):
@@ -422,10 +438,11 @@ def main():
     cpu = None
     accuracy = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        v, cores, dt = cpu_baseline_run(cfg, n, mode)
+        v, cores, dt, single = cpu_baseline_run(cfg, n, mode)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"the full per-rank batch ({n} arcs of config {cfg}) once through oracle "
-                         f"(a) with OpenMP over {cores} threads ({dt:.2f} s)"}
+                         f"(a) with OpenMP over {cores} threads ({dt:.2f} s)",
+               "single_thread_value": single, "cpu_model": cpu_model()}
         accuracy = accuracy_sample(a, b, z0, out, cnt, ref_out, ref_cnt, mode, ref_mode)
     del ref_out, ref_cnt
 
