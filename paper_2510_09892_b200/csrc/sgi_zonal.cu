@@ -37,6 +37,9 @@ namespace {
 #ifndef SGI_ZONAL_THREADS
 #define SGI_ZONAL_THREADS 256
 #endif
+#ifndef SGI_ZONAL_FILTER_MINB
+#define SGI_ZONAL_FILTER_MINB 1
+#endif
 constexpr int kThreads = SGI_ZONAL_THREADS;       // threads per CTA
 constexpr int kEdges = 2 * kThreads;              // edges per tile (two adjacent per thread)
 constexpr int kLatSmem = 4096;                    // latitude tables up to this length live in smem
@@ -181,7 +184,7 @@ __device__ __forceinline__ unsigned long long block_scan(unsigned long long v,
 // flight while it works on this one.  SMEM: the latitude table fits in shared memory (the
 // searches then compile to LDS).
 template <bool SMEM>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, SGI_ZONAL_FILTER_MINB)
 sgi_zonal_filter_kernel(const double* __restrict__ va, const double* __restrict__ vb, int64_t ne,
                         int64_t lde, const double* __restrict__ lat, int nlat,
                         int2* __restrict__ cand, unsigned long long* __restrict__ tile_sum) {

@@ -14,8 +14,9 @@ sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "build", "zvariants")
 VARIANTS = {
     "t256": {},
-    "t128": {"SGI_ZONAL_THREADS": 128},
-    "t64": {"SGI_ZONAL_THREADS": 64},
+    "f_minb4": {"SGI_ZONAL_FILTER_MINB": 4},
+    "f_minb5": {"SGI_ZONAL_FILTER_MINB": 5},
+    "f_minb6": {"SGI_ZONAL_FILTER_MINB": 6},
 }
 
 
