@@ -17,7 +17,7 @@ OUT = os.path.join(ROOT, "build", "variants")
 
 VARIANTS = {
     "base": {},
-    "tma_store": {'SGI_EFT_TMA_STORE': 1},
+    "fmad_true": {"FMAD": 1},
 }
 
 
@@ -26,9 +26,12 @@ def build():
     os.makedirs(OUT, exist_ok=True)
     src = os.path.join(ROOT, "paper_2510_09892_b200", "csrc", "sgi_capi.cu")
     for name, defs in VARIANTS.items():
-        d = [f"-D{k}={v}" for k, v in defs.items()]
+        flags = list(NVCC_FLAGS)
+        if defs.get("FMAD"):                       # contraction allowed (the intrinsics must not care)
+            flags = [f for f in flags if f != "-fmad=false"] + ["-fmad=true"]
+        d = [f"-D{k}={v}" for k, v in defs.items() if k != "FMAD"]
         lib = os.path.join(OUT, f"libsgi_{name}.so")
-        r = subprocess.run(["nvcc", *NVCC_FLAGS, *d, "-I", os.path.join(ROOT, "include"), "-o",
+        r = subprocess.run(["nvcc", *flags, *d, "-I", os.path.join(ROOT, "include"), "-o",
                             lib, src], capture_output=True, text=True)
         assert r.returncode == 0, r.stderr
         regs = [l.strip() for l in r.stderr.splitlines() if "registers" in l or "spill" in l]
@@ -65,7 +68,7 @@ def time_all(n, rounds=7, reps=20, config=2):
         f.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int64] * 2 + [ctypes.c_void_p] * 2 + \
             [ctypes.c_int, ctypes.c_void_p]
         fns[name] = f
-    modes = (1,)
+    modes = tuple(int(m) for m in os.environ.get("SGI_VARIANT_MODES", "1").split(","))
     times = {(v, m): [] for v in VARIANTS for m in modes}
     eff = {(v, m): [] for v in VARIANTS for m in modes}
     clocks = []
