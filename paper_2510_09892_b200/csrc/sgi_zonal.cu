@@ -238,13 +238,15 @@ sgi_zonal_filter_kernel(const double* __restrict__ va, const double* __restrict_
 }
 
 // Pass 2: exclusive scan of the tile sums in place, the total to *d_total (one CTA).  Rounds of
-// kScanRound entries: a coalesced load into shared memory, a serial scan of 4 contiguous
-// entries per thread, a block scan of the thread totals, a coalesced store.
-constexpr int kScanThreads = 1024, kScanPer = 4, kScanRound = kScanThreads * kScanPer;
+// kScanRound entries (one round covers 12.8 M edges): a coalesced load of every entry into
+// shared memory at once, a serial scan of kScanPer contiguous entries per thread (odd stride, so
+// the 8-byte reads are bank-conflict free), a block scan of the thread totals, a coalesced store.
+constexpr int kScanThreads = 1024, kScanPer = 25, kScanRound = kScanThreads * kScanPer;
+constexpr size_t kScanSmem = (size_t)kScanRound * sizeof(unsigned long long);
 __global__ void __launch_bounds__(kScanThreads)
 sgi_zonal_scan_kernel(unsigned long long* __restrict__ tile_sum, int64_t ntiles,
                       unsigned long long* __restrict__ d_total) {
-  __shared__ unsigned long long s[kScanRound];
+  extern __shared__ unsigned long long s[];
   __shared__ unsigned long long s_warp[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   unsigned long long carry = 0;
@@ -255,12 +257,9 @@ sgi_zonal_scan_kernel(unsigned long long* __restrict__ tile_sum, int64_t ntiles,
       s[k * kScanThreads + tid] = i < ntiles ? tile_sum[i] : 0;
     }
     __syncthreads();
-    unsigned long long v[kScanPer], sum = 0;
+    unsigned long long sum = 0;
 #pragma unroll
-    for (int k = 0; k < kScanPer; ++k) {
-      v[k] = s[tid * kScanPer + k];
-      sum += v[k];
-    }
+    for (int k = 0; k < kScanPer; ++k) sum += s[tid * kScanPer + k];
     unsigned long long x = sum;                      // block scan of the thread totals
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -282,8 +281,9 @@ sgi_zonal_scan_kernel(unsigned long long* __restrict__ tile_sum, int64_t ntiles,
     unsigned long long run = carry + x - sum + (warp > 0 ? s_warp[warp - 1] : 0);
 #pragma unroll
     for (int k = 0; k < kScanPer; ++k) {
+      const unsigned long long v = s[tid * kScanPer + k];
       s[tid * kScanPer + k] = run;
-      run += v[k];
+      run += v;
     }
     const unsigned long long round_total = s_warp[31];
     __syncthreads();
@@ -521,7 +521,9 @@ sgi_status sgi_zonal_intersect(const double* va, const double* vb, int64_t n_edg
     sgi_zonal_filter_kernel<false><<<gf, kThreads, filter_smem, st>>>(va, vb, n_edges, ld_e, lat_z0,
                                                                       n_lat, cand, tile);
   }
-  sgi_zonal_scan_kernel<<<1, kScanThreads, 0, st>>>(tile, ntiles, d_total);
+  cudaFuncSetAttribute(sgi_zonal_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)kScanSmem);
+  sgi_zonal_scan_kernel<<<1, kScanThreads, kScanSmem, st>>>(tile, ntiles, d_total);
   if (cap > 0) {
     auto emit = [&](auto kernel) {
       const int ge = grid_for(kernel, emit_smem);
