@@ -105,7 +105,8 @@ sgi_status sgi_count_histogram(const uint8_t* out_count, int64_t n,
  * sgi_intersect_arc_lat on (va_e, vb_e, lat_z0[k]) in `mode`.  Pairs j >= cap are not written;
  * *d_total (device) receives the number of candidate pairs, so cap = 0 is a count-only call.
  * d_work: caller-owned device workspace of sgi_zonal_workspace_bytes(n_edges) bytes (8 B per
- * edge for its candidate range plus 8 B per 512-edge tile, plus 8 B).  n_lat <= 2^23.
+ * edge for its candidate range plus 8 B per 512-edge tile, plus 8 B), 16-byte aligned
+ * (SGI_E_INVALID otherwise; cudaMalloc and PyTorch allocations are).  n_lat <= 2^23.
  * Asynchronous on `stream` (three launches: filter, scan, emit).  Errors as for
  * sgi_intersect_arc_lat. */
 sgi_status sgi_zonal_intersect(const double* va, const double* vb, int64_t n_edges,

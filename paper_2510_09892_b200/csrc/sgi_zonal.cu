@@ -9,16 +9,14 @@
 //          a search in the latitude table (shared memory) gives the candidate latitudes
 //          [klo, klo + kcnt), stored per edge (8 B) with each tile's candidate sum;
 //   scan   one CTA turns the tile sums into output bases (and the total);
-//   emit   CTAs walk tiles in any order (each tile knows its base): a block scan of the stored
-//          kcnt orders the tile's candidates (edge-major, latitude ascending, deterministic)
-//          and compacts the candidate edges; only those are read again, one per thread, and
-//          get the query's z0-independent AccuX head (accurate normal pairs, |n_xy|^2, |n|^2 —
-//          lines 2-6), staged in shared memory; the tile's pairs are then processed
-//          densely (pair c -> thread c mod kThreads,
-//          so lanes are not idle on edges that span no latitude), running the z0-dependent tail
-//          of the query (AccuX lines 7-25 + containment).
-// A pair's result is bit-identical to sgi_intersect_arc_lat on the same (a, b, z0): head and
-// tail are the same device code.  Candidate pairs whose latitude only touches the widened range
+//   emit   warps walk tiles in any order (each tile knows its base), 128 edges at a time: a
+//          warp scan of the stored kcnt numbers the segment's pairs (edge-major, latitude
+//          ascending, deterministic), each pair's endpoints are gathered by cp.async into a
+//          warp-private queue, and every 64 queued pairs run as 32 two-query lanes of the
+//          batch kernel's W2 path (AccuX lines 2-25 + containment) while the other queue's
+//          gathers are in flight; no CTA barriers.
+// A pair's result is bit-identical to sgi_intersect_arc_lat on the same (a, b, z0): both run
+// the same device code.  Candidate pairs whose latitude only touches the widened range
 // come out with count 0; every pair with a nonzero count is a candidate (tests/test_gpu_zonal.py).
 #include <cuda_runtime.h>
 
@@ -150,34 +148,6 @@ __device__ __forceinline__ void candidates(const double* x, const double* tab, c
 }
 
 
-// Block-wide inclusive scan of one 64-bit value per thread (kThreads threads); returns the
-// inclusive value and leaves the block total in *total.
-__device__ __forceinline__ unsigned long long block_scan(unsigned long long v,
-                                                         unsigned long long* s_warp,
-                                                         unsigned long long* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const unsigned long long y = __shfl_up_sync(0xffffffffu, v, d);
-    if (lane >= d) v += y;
-  }
-  if (lane == 31) s_warp[warp] = v;
-  __syncthreads();
-  if (warp == 0) {
-    unsigned long long w = lane < kThreads / 32 ? s_warp[lane] : 0;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const unsigned long long y = __shfl_up_sync(0xffffffffu, w, d);
-      if (lane >= d) w += y;
-    }
-    if (lane < kThreads / 32) s_warp[lane] = w;
-  }
-  __syncthreads();
-  const unsigned long long incl = v + (warp > 0 ? s_warp[warp - 1] : 0);
-  *total = s_warp[kThreads / 32 - 1];
-  return incl;
-}
-
 // Pass 1: candidate latitudes of every edge, cand[e] = (klo, kcnt), and each tile's sum.
 // Persistent CTAs stride over the tiles (the latitude table and its bucket index are staged
 // once per CTA); thread tid owns edges 2 tid and 2 tid + 1 of a tile, the next tile's loads in
@@ -298,71 +268,18 @@ sgi_zonal_scan_kernel(unsigned long long* __restrict__ tile_sum, int64_t ntiles,
   if (tid == 0) *d_total = carry;
 }
 
-// Pass 3: emit every candidate pair of each tile at its ordered output slot.
-//
-// Each tile's endpoint planes and candidate ranges are staged in shared memory by cp.async one
-// tile ahead (double buffer), so the compute never waits on a gather.  A block scan of the
-// stored kcnt compacts the tile's candidate edges in edge order; then, when every candidate
-// spans at most kFuseMax latitudes (the common case: mesh edges are short), one thread per
-// candidate runs the query's z0-independent AccuX head (lines 2-6) once and the z0-dependent
-// tail (lines 7-25 + containment) for each of its latitudes.  Tiles with a long candidate range
-// process their pairs densely instead (pair c -> thread c mod kThreads, head recomputed per
-// pair), so no lane idles behind one long edge.
-constexpr int kFuseMax = 4;
-struct EmitStage {                 // one tile's inputs
-  double x[6][kEdges];             // endpoint planes a_x, a_y, a_z, b_x, b_y, b_z
-  int2 cand[kEdges];               // (klo, kcnt) per edge
-};
-struct EmitList {                  // the tile's compacted candidate edges
-  int edge[kEdges];                // tile-local edge index of candidate c
-  int klo[kEdges];                 // first candidate latitude of candidate c
-  int kcnt[kEdges];                // number of candidate latitudes of candidate c
-  long long off[kEdges];           // first pair of candidate c within the tile
-};
-struct EmitSmem {
-  EmitStage stage[2];
-  EmitList list[2];
-};
-
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src)
                : "memory");
 }
 
-// Thread tid stages edges 2 tid, 2 tid + 1 of tile t (those below ne) and commits the group.
-__device__ __forceinline__ void stage_tile(EmitStage& S, int64_t t, int64_t ne, int64_t lde,
-                                           const double* __restrict__ va,
-                                           const double* __restrict__ vb,
-                                           const int2* __restrict__ cand) {
-  const int l0 = 2 * threadIdx.x;
-#pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    const int64_t e = t * kEdges + l0 + j;
-    if (e < ne) {
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        cp_async8(&S.x[c][l0 + j], va + c * lde + e);
-        cp_async8(&S.x[3 + c][l0 + j], vb + c * lde + e);
-      }
-      cp_async8(&S.cand[l0 + j], cand + e);
-    }
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-
-template <int MODE, class IN>
-__device__ __forceinline__ void emit_pair(const sgi::EdgePre& pre, const IN& in, int64_t edge,
-                                          int k, const double* tab, int64_t j, int64_t cap,
-                                          int64_t* __restrict__ out_edge,
-                                          int32_t* __restrict__ out_lat,
-                                          uint8_t* __restrict__ out_count,
-                                          double* __restrict__ out_xyz) {
-  const double z0 = tab[k];
-  sgi::QueryOut o;
-  if (!sgi::lat_query<MODE, sgi::Fast>(pre, in, z0, o)) {
-    const sgi::RegIn r = {{in(0), in(1), in(2), in(3), in(4), in(5)}};
-    sgi::query_exact<MODE>(r, z0, o);
-  }
+// Pair j of the output: (edge, k), its count and both slots (unused slots: canonical NaN).
+__device__ __forceinline__ void store_pair(const sgi::QueryOut& o, double z0, int64_t edge, int k,
+                                           int64_t j, int64_t cap,
+                                           int64_t* __restrict__ out_edge,
+                                           int32_t* __restrict__ out_lat,
+                                           uint8_t* __restrict__ out_count,
+                                           double* __restrict__ out_xyz) {
   const bool deg = o.count == sgi::kDegenerate;
   const double nan = sgi::qnan();
   out_edge[j] = edge;
@@ -376,84 +293,216 @@ __device__ __forceinline__ void emit_pair(const sgi::EdgePre& pre, const IN& in,
   __stcs(out_xyz + 5 * cap + j, (!deg && o.count == 2) ? z0 : nan);
 }
 
+// Pass 3: emit every candidate pair at its ordered output slot; no CTA barriers.  Each warp owns whole 512-edge tiles (grid
+// stride over warps) and walks them kSegEdges = 128 edges at a time; lane L owns the four
+// adjacent edges 4L .. 4L + 3 (candidate ranges prefetched one segment ahead in registers,
+// their kcnt summed locally, one warp scan per segment) and appends their pairs, in output
+// order, to a warp-private queue laid out for two-query lanes: item i sits in column i mod 32,
+// half i / 32, so lane L later reads items L and L + 32 with one 128-bit shared load per
+// coordinate (SmemIn2, the same W2 path as the batch kernel) and the output stores stay
+// coalesced.  Endpoints are gathered into the queue by cp.async as pairs are appended; two
+// queues alternate, so one queue's gathers fly while the other is computed.  The head is
+// recomputed for every pair (mesh edges rarely span two latitudes); a long candidate range
+// just fills several queues, so lanes stay balanced.
+#ifndef SGI_ZONAL_WTHREADS
+#define SGI_ZONAL_WTHREADS 256   // 2 CTAs per SM (0.489 ms per C4 pass vs 0.496 at 512)
+#endif
+constexpr int kWThreads = SGI_ZONAL_WTHREADS, kWarpsPerCta = kWThreads / 32, kBatch = 64;
+constexpr int kSegEdges = 128;
+static_assert(kEdges % kSegEdges == 0, "a tile is a whole number of segments");
+struct WarpQueue {
+  double v[7][32][2];              // planes a_x .. b_z, z0; [column][half]
+  long long edge[kBatch];
+  long long slot[kBatch];
+  int lat[kBatch];
+};
+struct WarpSmem {
+  WarpQueue q[2];
+};
+
+// Rare path: pair (e, k) recomputed from HBM with the IEEE intrinsics and stored at slot j.
+// Out of line so the fast path carries none of its state.
+template <int MODE>
+__device__ __noinline__ void emit_exact(const double* __restrict__ va,
+                                        const double* __restrict__ vb, int64_t lde,
+                                        const double* tab, int64_t e, int k, int64_t j,
+                                        int64_t cap, int64_t* __restrict__ out_edge,
+                                        int32_t* __restrict__ out_lat,
+                                        uint8_t* __restrict__ out_count,
+                                        double* __restrict__ out_xyz) {
+  const sgi::RegIn r = {{va[e], va[lde + e], va[2 * lde + e], vb[e], vb[lde + e], vb[2 * lde + e]}};
+  const double z0 = tab[k];
+  sgi::QueryOut o;
+  sgi::query_exact<MODE>(r, z0, o);
+  store_pair(o, z0, e, k, j, cap, out_edge, out_lat, out_count, out_xyz);
+}
+
+// One queue of n <= kBatch pairs: lane runs items lane and lane + 32 as one W2 query pair (EFT
+// modes) or one after the other.  Items >= n are stale or unset and are never stored.
+template <int MODE>
+__device__ __forceinline__ void run_batch(const WarpQueue& q, int n, const double* tab,
+                                          const double* __restrict__ va,
+                                          const double* __restrict__ vb, int64_t lde,
+                                          int64_t cap, int64_t* __restrict__ out_edge,
+                                          int32_t* __restrict__ out_lat,
+                                          uint8_t* __restrict__ out_count,
+                                          double* __restrict__ out_xyz) {
+  const int lane = threadIdx.x & 31;
+  const sgi::SmemIn2 in = {smem_u32(&q.v[0][lane][0]), (uint32_t)sizeof(q.v[0])};
+  const sgi::W2 zz = in(6);
+  auto store = [&](const sgi::QueryOut& o, double z0, bool ok, int r) {
+    if (r >= n) return;
+    const int64_t j = q.slot[r];
+    if (j >= cap) return;
+    if (ok) store_pair(o, z0, q.edge[r], q.lat[r], j, cap, out_edge, out_lat, out_count, out_xyz);
+    else emit_exact<MODE>(va, vb, lde, tab, q.edge[r], q.lat[r], j, cap, out_edge, out_lat,
+                          out_count, out_xyz);
+  };
+  if constexpr (MODE == sgi::MODE_EFT || MODE == sgi::MODE_EFT_LITERAL) {
+    sgi::QueryOut2 o;
+    const sgi::B2 ok = sgi::query_fast2<MODE>(in, zz, o);
+    store({o.p0x.x, o.p0y.x, o.p1x.x, o.p1y.x, o.count[0]}, zz.x, ok.x, lane);
+    store({o.p0x.y, o.p0y.y, o.p1x.y, o.p1y.y, o.count[1]}, zz.y, ok.y, lane + 32);
+  } else {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const sgi::SmemIn in1 = {smem_u32(&q.v[0][lane][h]), (uint32_t)sizeof(q.v[0])};
+      const double z0 = in1(6);
+      sgi::QueryOut o;
+      const bool ok = sgi::query_fast<MODE>(in1, z0, o);
+      store(o, z0, ok, lane + 32 * h);
+    }
+  }
+}
+
 template <int MODE, bool SMEM>
-__global__ void __launch_bounds__(kThreads, 512 / kThreads)
-sgi_zonal_emit_kernel(const double* __restrict__ va, const double* __restrict__ vb, int64_t ne,
-                      int64_t lde, const double* __restrict__ lat, int nlat, int64_t cap,
-                      int64_t* __restrict__ out_edge, int32_t* __restrict__ out_lat,
-                      uint8_t* __restrict__ out_count, double* __restrict__ out_xyz,
-                      const int2* __restrict__ cand,
-                      const unsigned long long* __restrict__ tile_base) {
+__global__ void __launch_bounds__(kWThreads, 512 / kWThreads)
+sgi_zonal_emit_warp_kernel(const double* __restrict__ va, const double* __restrict__ vb,
+                           int64_t ne, int64_t lde, const double* __restrict__ lat, int nlat,
+                           int64_t cap, int64_t* __restrict__ out_edge,
+                           int32_t* __restrict__ out_lat, uint8_t* __restrict__ out_count,
+                           double* __restrict__ out_xyz, const int2* __restrict__ cand,
+                           const unsigned long long* __restrict__ tile_base) {
   extern __shared__ __align__(16) double s_dyn[];
-  __shared__ unsigned long long s_warp[kThreads / 32];
-  const int tid = threadIdx.x;
   const size_t lat_words = SMEM ? ((size_t)nlat + 1) / 2 * 2 : 0;
-  EmitSmem& S = *reinterpret_cast<EmitSmem*>(s_dyn + lat_words);
   if (SMEM) {
-    for (int k = threadIdx.x; k < nlat; k += kThreads) s_dyn[k] = lat[k];
+    for (int k = threadIdx.x; k < nlat; k += kWThreads) s_dyn[k] = lat[k];
     __syncthreads();
   }
   const double* tab = SMEM ? s_dyn : lat;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WarpSmem& W = reinterpret_cast<WarpSmem*>(s_dyn + lat_words)[warp];
+  // this warp's tiles t0, t0 + nwarps, ... (grid stride: at any time the warps of the grid
+  // work on neighbouring tiles, which measured faster than contiguous per-warp ranges)
   const int64_t ntiles = (ne + kEdges - 1) / kEdges;
-  int buf = 0;
-  if ((int64_t)blockIdx.x < ntiles) stage_tile(S.stage[0], blockIdx.x, ne, lde, va, vb, cand);
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, buf ^= 1) {
-    asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's copies of tile t
-    EmitStage& G = S.stage[buf];
-    EmitList& L = S.list[buf];
-    const int64_t base = (int64_t)tile_base[t];
-    const int l0 = 2 * tid;
-    const int64_t e0 = t * kEdges + l0;
-    const int2 c0 = e0 < ne ? G.cand[l0] : make_int2(0, 0);
-    const int2 c1 = e0 + 1 < ne ? G.cand[l0 + 1] : make_int2(0, 0);
-    // pairs (high 40 bits) and candidate flags (low 24 bits) of this thread's two edges
-    const unsigned long long pairs = (unsigned long long)(unsigned)c0.y + (unsigned)c1.y;
-    const unsigned flags = (c0.y > 0) + (c1.y > 0);
-    const unsigned long long mine = (pairs << 24) | flags;
-    unsigned long long tot;
-    const unsigned long long excl = block_scan(mine, s_warp, &tot) - mine;  // (barriers)
-    const int ncand = (int)(tot & 0xFFFFFF);
-    const int64_t npairs = (int64_t)(tot >> 24);
-    int slot = (int)(excl & 0xFFFFFF);
-    int64_t poff = (int64_t)(excl >> 24);
-    if (c0.y > 0) {
-      L.edge[slot] = l0; L.klo[slot] = c0.x; L.kcnt[slot] = c0.y; L.off[slot] = poff; ++slot;
-    }
-    poff += c0.y;
-    if (c1.y > 0) { L.edge[slot] = l0 + 1; L.klo[slot] = c1.x; L.kcnt[slot] = c1.y; L.off[slot] = poff; }
-    // the list is complete, every thread's tile-t data is visible, and every thread is done
-    // with tile t - gridDim.x, whose buffer the next tile's copies now overwrite
-    const bool dense = __syncthreads_or(c0.y > kFuseMax || c1.y > kFuseMax);
-    const int64_t tn = t + gridDim.x;
-    if (tn < ntiles) stage_tile(S.stage[buf ^ 1], tn, ne, lde, va, vb, cand);
-    const uint32_t gx = smem_u32(&G.x[0][0]);
-    if (!dense) {
-      for (int c = tid; c < ncand; c += kThreads) {     // head once, then its latitudes
-        const int le = L.edge[c];
-        const sgi::SmemIn in = {gx + (uint32_t)le * 8u, (uint32_t)(kEdges * 8)};
-        const sgi::EdgePre pre = sgi::edge_pre<MODE>(in);
-        const int kc = L.kcnt[c], k0 = L.klo[c];
-        const int64_t j0 = base + L.off[c];
-        for (int q = 0; q < kc && j0 + q < cap; ++q)
-          emit_pair<MODE>(pre, in, t * kEdges + le, k0 + q, tab, j0 + q, cap, out_edge, out_lat,
-                          out_count, out_xyz);
-      }
+  const int64_t t0 = (int64_t)blockIdx.x * kWarpsPerCta + warp;
+  const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerCta;
+  const int mytiles = t0 < ntiles ? (int)((ntiles - t0 + nwarps - 1) / nwarps) : 0;
+  constexpr int kSegs = kEdges / kSegEdges;
+  const int nseg = mytiles * kSegs;                    // this warp's segments, in order
+  const int l0 = 4 * lane;
+  auto seg_edge0 = [&](int g) {
+    return (t0 + (int64_t)(g / kSegs) * nwarps) * kEdges + (g % kSegs) * kSegEdges;
+  };
+  auto load_cand = [&](int g, int4& a, int4& b) {      // lane's four (klo, kcnt), 0 beyond ne
+    a = make_int4(0, 0, 0, 0);
+    b = a;
+    if (g >= nseg) return;
+    const int64_t e = seg_edge0(g) + l0;
+    if (e + 3 < ne) {
+      a = __ldg(reinterpret_cast<const int4*>(cand + e));
+      b = __ldg(reinterpret_cast<const int4*>(cand + e + 2));
     } else {
-      for (int64_t p = tid; p < npairs && base + p < cap; p += kThreads) {
-        int l = 0, h = ncand;                            // owner candidate: last off[l] <= p
-        while (h - l > 1) {
-          const int mid = (l + h) >> 1;
-          if (L.off[mid] <= p) l = mid; else h = mid;
+      if (e < ne) { const int2 c = cand[e]; a.x = c.x; a.y = c.y; }
+      if (e + 1 < ne) { const int2 c = cand[e + 1]; a.z = c.x; a.w = c.y; }
+      if (e + 2 < ne) { const int2 c = cand[e + 2]; b.x = c.x; b.y = c.y; }
+    }
+  };
+  int4 na, nb;
+  load_cand(0, na, nb);
+  unsigned long long nbase = nseg > 0 ? tile_base[t0] : 0;
+  int cur = 0, qn = 0;                                 // filling queue, its queued pairs
+  bool pending = false;                                // queue cur ^ 1 gathered, not yet run
+  int64_t base = 0;                                    // first slot of the current segment
+  for (int g = 0; g < nseg; ++g) {
+    const int4 ca = na, cb = nb;
+    const int64_t e0 = seg_edge0(g);
+    if (g % kSegs == 0) base = (int64_t)nbase;
+    load_cand(g + 1, na, nb);                          // prefetch the next segment
+    if ((g + 1) % kSegs == 0 && g + 1 < nseg)
+      nbase = tile_base[t0 + (int64_t)((g + 1) / kSegs) * nwarps];
+    const unsigned k0 = (unsigned)ca.y, k1 = (unsigned)ca.w, k2 = (unsigned)cb.y;
+    const unsigned mine = k0 + k1 + k2 + (unsigned)cb.w;
+    unsigned incl = mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += y;
+    }
+    const unsigned excl = incl - mine;
+    const unsigned segtot = __shfl_sync(0xffffffffu, incl, 31);
+    for (unsigned cursor = 0; cursor < segtot;) {      // queue slots [qn, qn + m) <- pairs [cursor, ...)
+      const unsigned m = min((unsigned)(kBatch - qn), segtot - cursor);
+      WarpQueue& q = W.q[cur];
+      // slot-major fill: lane L fills slots L and L + 32; pair p's owner lane is the last lane
+      // with excl <= p (found by a shuffle binary search), then one of its four edges
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int at = lane + 32 * h;
+        const bool valid = at >= qn && at < qn + (int)m;
+        const unsigned p = min(cursor + (unsigned)(at - qn), segtot - 1);   // clamped when idle
+        int own = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+          const unsigned x = __shfl_sync(0xffffffffu, excl, own + step);
+          if (x <= p) own += step;
         }
-        const int le = L.edge[l];
-        const sgi::SmemIn in = {gx + (uint32_t)le * 8u, (uint32_t)(kEdges * 8)};
-        emit_pair<MODE>(sgi::edge_pre<MODE>(in), in, t * kEdges + le,
-                        L.klo[l] + (int)(p - L.off[l]), tab, base + p, cap, out_edge, out_lat,
-                        out_count, out_xyz);
+        unsigned off = p - __shfl_sync(0xffffffffu, excl, own);
+        const unsigned o0 = __shfl_sync(0xffffffffu, k0, own);
+        const unsigned o1 = __shfl_sync(0xffffffffu, k1, own);
+        const unsigned o2 = __shfl_sync(0xffffffffu, k2, own);
+        const int q0 = __shfl_sync(0xffffffffu, ca.x, own), q1 = __shfl_sync(0xffffffffu, ca.z, own);
+        const int q2 = __shfl_sync(0xffffffffu, cb.x, own), q3 = __shfl_sync(0xffffffffu, cb.z, own);
+        int i = 0, klo = q0;                           // the owner's edge holding pair p
+        if (off >= o0) { off -= o0; i = 1; klo = q1;
+          if (off >= o1) { off -= o1; i = 2; klo = q2;
+            if (off >= o2) { off -= o2; i = 3; klo = q3; } } }
+        if (valid) {
+          const int64_t e = e0 + 4 * own + i;
+          const int k = klo + (int)off;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            cp_async8(&q.v[c][lane][h], va + c * lde + e);
+            cp_async8(&q.v[3 + c][lane][h], vb + c * lde + e);
+          }
+          q.v[6][lane][h] = tab[k];
+          q.edge[at] = e;
+          q.lat[at] = k;
+          q.slot[at] = base + p;
+        }
+      }
+      qn += (int)m;
+      cursor += m;
+      if (qn == kBatch) {                              // queue cur is full: run the other one
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (pending) {
+          asm volatile("cp.async.wait_group 1;" ::: "memory");
+          run_batch<MODE>(W.q[cur ^ 1], kBatch, tab, va, vb, lde, cap, out_edge, out_lat,
+                          out_count, out_xyz);
+        }
+        pending = true;
+        cur ^= 1;
+        qn = 0;
       }
     }
+    base += segtot;
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
   asm volatile("cp.async.wait_all;" ::: "memory");
+  if (pending)
+    run_batch<MODE>(W.q[cur ^ 1], kBatch, tab, va, vb, lde, cap, out_edge, out_lat, out_count,
+                    out_xyz);
+  if (qn > 0) run_batch<MODE>(W.q[cur], qn, tab, va, vb, lde, cap, out_edge, out_lat, out_count, out_xyz);
 }
 
 }  // namespace
@@ -478,9 +527,10 @@ sgi_status sgi_zonal_intersect(const double* va, const double* vb, int64_t n_edg
     return SGI_E_INVALID;
   }
   if (n_edges > 0 && (!va || !vb || (n_lat > 0 && !lat_z0) || !d_work ||
+                      ((uintptr_t)d_work & 15) != 0 ||
                       work_bytes < sgi_zonal_workspace_bytes(n_edges))) {
-    sgi_internal::set_error_msg("sgi_zonal_intersect: null pointer or workspace too small",
-                                cudaSuccess);
+    sgi_internal::set_error_msg(
+        "sgi_zonal_intersect: null pointer, workspace not 16-B aligned or too small", cudaSuccess);
     return SGI_E_INVALID;
   }
   if (cap > 0 && (!out_edge || !out_lat || !out_count || !out_xyz)) {
@@ -498,7 +548,6 @@ sgi_status sgi_zonal_intersect(const double* va, const double* vb, int64_t n_edg
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t lat_smem = n_lat <= kLatSmem ? (size_t)n_lat * sizeof(double) : 0;
   const size_t lat_smem_even = n_lat <= kLatSmem ? ((size_t)n_lat + 1) / 2 * 2 * sizeof(double) : 0;
-  const size_t emit_smem = lat_smem_even + sizeof(EmitSmem);
   const int64_t ntiles = (n_edges + kEdges - 1) / kEdges;
   int2* cand = (int2*)d_work;
   unsigned long long* tile = (unsigned long long*)((char*)d_work + (size_t)n_edges * sizeof(int2));
@@ -526,11 +575,17 @@ sgi_status sgi_zonal_intersect(const double* va, const double* vb, int64_t n_edg
   sgi_zonal_scan_kernel<<<1, kScanThreads, kScanSmem, st>>>(tile, ntiles, d_total);
   if (cap > 0) {
     auto emit = [&](auto kernel) {
-      const int ge = grid_for(kernel, emit_smem);
-      kernel<<<ge, kThreads, emit_smem, st>>>(va, vb, n_edges, ld_e, lat_z0, n_lat, cap, out_edge,
-                                              out_lat, out_count, out_xyz, cand, tile);
+      int occ = 1;
+      const size_t smem = lat_smem_even + kWarpsPerCta * sizeof(WarpSmem);
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kWThreads, smem);
+      const int64_t want = (ntiles + kWarpsPerCta - 1) / kWarpsPerCta;
+      const int64_t g = (int64_t)sms * (occ < 1 ? 1 : occ);
+      kernel<<<(int)(g < want ? g : want), kWThreads, smem, st>>>(
+          va, vb, n_edges, ld_e, lat_z0, n_lat, cap, out_edge, out_lat, out_count, out_xyz, cand,
+          tile);
     };
-#define SGI_EMIT(M) (smem_tab ? emit(sgi_zonal_emit_kernel<M, true>) : emit(sgi_zonal_emit_kernel<M, false>))
+#define SGI_EMIT(M) (smem_tab ? emit(sgi_zonal_emit_warp_kernel<M, true>) : emit(sgi_zonal_emit_warp_kernel<M, false>))
     switch (mode) {
       case SGI_MODE_NAIVE: SGI_EMIT(sgi::MODE_NAIVE); break;
       case SGI_MODE_EFT: SGI_EMIT(sgi::MODE_EFT); break;

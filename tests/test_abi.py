@@ -86,6 +86,9 @@ def test_zonal_validates_arguments(lib):
     assert lib.sgi_zonal_intersect(e.ctypes.data, e.ctypes.data, 8, 8, lat.ctypes.data, 4, 0,
                                    None, None, None, None, tot.ctypes.data, None, 0, 1,
                                    None) == sgi.SGI_E_INVALID          # no workspace
+    assert lib.sgi_zonal_intersect(e.ctypes.data, e.ctypes.data, 8, 8, lat.ctypes.data, 4, 0,
+                                   None, None, None, None, tot.ctypes.data, 0x10008, 1 << 20, 1,
+                                   None) == sgi.SGI_E_INVALID          # workspace not 16-B aligned
     assert sgi.zonal_workspace_bytes(0) == 8                       # the tile-sum terminator
     assert sgi.zonal_workspace_bytes(1000) == 1000 * 8 + (2 + 1) * 8   # 512-edge tiles
     assert sgi.zonal_workspace_bytes(-1) == 0

@@ -1,7 +1,7 @@
 """Build and time launch-shape variants of the fused zonal pass (tools, not product).
     python tools/zonal_variants.py build      # here
     python tools/zonal_variants.py time       # on the GPU: C4 mesh x 1,800 latitudes
-Knobs: SGI_ZONAL_THREADS (tile = 2x edges), SGI_ZONAL_FUSE, SGI_ZONAL_EMIT_MINB."""
+Knobs: SGI_ZONAL_THREADS (tile = 2x edges), SGI_ZONAL_FUSE, SGI_ZONAL_WTHREADS (emit CTA size)."""
 import ctypes
 import json
 import os
@@ -13,10 +13,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "build", "zvariants")
 VARIANTS = {
-    "t256": {},
-    "f_minb4": {"SGI_ZONAL_FILTER_MINB": 4},
-    "f_minb5": {"SGI_ZONAL_FILTER_MINB": 5},
-    "f_minb6": {"SGI_ZONAL_FILTER_MINB": 6},
+    "emit_t256": {},
+    "emit_t512": {"SGI_ZONAL_WTHREADS": 512},
 }
 
 
