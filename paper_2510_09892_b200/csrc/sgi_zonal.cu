@@ -25,6 +25,7 @@
 
 #include "sgi.h"
 #include "sgi_query.cuh"
+#include "sgi_tma.cuh"
 
 namespace sgi_internal {
 void set_error_msg(const char* msg, cudaError_t e);   // sgi_capi.cu: sgi_last_error() text
@@ -35,8 +36,12 @@ namespace {
 #ifndef SGI_ZONAL_THREADS
 #define SGI_ZONAL_THREADS 256
 #endif
+#ifndef SGI_ZONAL_FILTER_PREFETCH
+#define SGI_ZONAL_FILTER_PREFETCH 0   // 1: the next tile's edges load into registers during this
+                                      // one (110 regs, 2 CTAs/SM; 3 CTAs/SM without: 0.480 vs 0.483 ms)
+#endif
 #ifndef SGI_ZONAL_FILTER_MINB
-#define SGI_ZONAL_FILTER_MINB 1
+#define SGI_ZONAL_FILTER_MINB 3     // 80 regs: 24 warps/SM (the filter is latency-bound)
 #endif
 constexpr int kThreads = SGI_ZONAL_THREADS;       // threads per CTA
 constexpr int kEdges = 2 * kThreads;              // edges per tile (two adjacent per thread)
@@ -61,9 +66,6 @@ __device__ __forceinline__ int upper_bound(const double* t, int n, double x) {  
   return lo;
 }
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
 
 // A bucket index over z in [-1, 1] turns each table search into one shared-memory lookup plus a
 // short binary search: bkt[b] = lower_bound(tab, -1 + 2b/kBuckets) for b = 0..kBuckets (the
@@ -143,7 +145,16 @@ __device__ __forceinline__ void candidates(const double* x, const double* tab, c
     kcnt = nlat;                                     // n = 0: degenerate at every latitude
   } else if (zhi == zhi && zlo == zlo) {             // NaN inputs: no candidates
     klo = bucket_search<false>(bkt, tab, nlat, __dsub_rn(zlo, kDelta));
-    kcnt = bucket_search<true>(bkt, tab, nlat, __dadd_rn(zhi, kDelta)) - klo;
+    // first k with tab[k] > zhi + delta: mesh edges span a latitude or two, so step from klo
+    // and search only past kStep entries (the same index either way)
+    const double top = __dadd_rn(zhi, kDelta);
+    constexpr int kStep = 3;
+    int k = klo;
+#pragma unroll
+    for (int s = 0; s < kStep; ++s)
+      if (k < nlat && tab[k] <= top) ++k;
+    if (k == klo + kStep && k < nlat && tab[k] <= top) k = bucket_search<true>(bkt, tab, nlat, top);
+    kcnt = k - klo;
   }
 }
 
@@ -159,7 +170,7 @@ sgi_zonal_filter_kernel(const double* __restrict__ va, const double* __restrict_
                         int64_t lde, const double* __restrict__ lat, int nlat,
                         int2* __restrict__ cand, unsigned long long* __restrict__ tile_sum) {
   extern __shared__ __align__(16) double s_lat[];
-  __shared__ unsigned long long s_red[kThreads / 32];
+  __shared__ unsigned s_red[2][kThreads / 32];
   __shared__ int s_bkt[kBuckets + 1];
   if (SMEM) {
     for (int k = threadIdx.x; k < nlat; k += kThreads) s_lat[k] = lat[k];
@@ -168,20 +179,21 @@ sgi_zonal_filter_kernel(const double* __restrict__ va, const double* __restrict_
   const double* tab = SMEM ? s_lat : lat;
   build_buckets(s_bkt, tab, nlat);
   const int64_t ntiles = (ne + kEdges - 1) / kEdges;
-  int64_t t = blockIdx.x;
-  EdgeX cur[2];
-#pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    const int64_t e = t * kEdges + 2 * threadIdx.x + j;
-    if (t < ntiles && e < ne) load_edge(cur[j], va, vb, lde, e);
-  }
-  for (; t < ntiles; t += gridDim.x) {
-    const int64_t e0 = t * kEdges + 2 * threadIdx.x, en = e0 + (int64_t)gridDim.x * kEdges;
-    EdgeX nxt[2];
+  const int64_t G = gridDim.x;
+  // tile t: candidates of the thread's two edges from `cur` while the edges of tile t + G load
+  // into `nxt`; per-warp sums (32-bit: <= 64 x 2^23) meet in s_red[parity] behind one barrier
+  auto step = [&](int64_t t, int parity, EdgeX (&cur)[2], EdgeX (&nxt)[2]) {
+    const int64_t e0 = t * kEdges + 2 * threadIdx.x, en = e0 + G * kEdges;
+#if SGI_ZONAL_FILTER_PREFETCH
 #pragma unroll
     for (int j = 0; j < 2; ++j)
       if (en + j < ne) load_edge(nxt[j], va, vb, lde, en + j);
-    unsigned long long sum = 0;
+#else
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      if (e0 + j < ne) load_edge(cur[j], va, vb, lde, e0 + j);
+#endif
+    unsigned sum = 0;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       if (e0 + j < ne) {
@@ -193,17 +205,25 @@ sgi_zonal_filter_kernel(const double* __restrict__ va, const double* __restrict_
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, d);
-    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = sum;
-    __syncthreads();
+    if ((threadIdx.x & 31) == 0) s_red[parity][threadIdx.x >> 5] = sum;
+    __syncthreads();        // also keeps warps within one tile, so s_red[parity] is free again
     if (threadIdx.x == 0) {
       unsigned long long acc = 0;
 #pragma unroll
-      for (int w = 0; w < kThreads / 32; ++w) acc += s_red[w];
+      for (int w = 0; w < kThreads / 32; ++w) acc += s_red[parity][w];
       tile_sum[t] = acc;
     }
-    __syncthreads();
-    cur[0] = nxt[0];
-    cur[1] = nxt[1];
+  };
+  EdgeX A[2], B[2];                                    // ping-pong: no register copies
+  int64_t t = blockIdx.x;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int64_t e = t * kEdges + 2 * threadIdx.x + j;
+    if (t < ntiles && e < ne) load_edge(A[j], va, vb, lde, e);
+  }
+  for (; t < ntiles; t += 2 * G) {
+    step(t, 0, A, B);
+    if (t + G < ntiles) step(t + G, 1, B, A);
   }
 }
 
@@ -310,14 +330,17 @@ __device__ __forceinline__ void store_pair(const sgi::QueryOut& o, double z0, in
 constexpr int kWThreads = SGI_ZONAL_WTHREADS, kWarpsPerCta = kWThreads / 32, kBatch = 64;
 constexpr int kSegEdges = 128;
 static_assert(kEdges % kSegEdges == 0, "a tile is a whole number of segments");
-struct WarpQueue {
-  double v[7][32][2];              // planes a_x .. b_z, z0; [column][half]
+struct alignas(16) WarpQueue {
+  double v[6][32][2];              // planes a_x .. b_z; [column][half]
   long long edge[kBatch];
   long long slot[kBatch];
   int lat[kBatch];
 };
-struct WarpSmem {
+constexpr int kCandRing = 3;       // candidate-range segments in flight per warp (bulk copies)
+struct alignas(16) WarpSmem {
   WarpQueue q[2];
+  int2 cand[kCandRing][kSegEdges];
+  uint64_t full[kCandRing];        // mbarrier per ring slot (bytes of the bulk copy)
 };
 
 // Rare path: pair (e, k) recomputed from HBM with the IEEE intrinsics and stored at slot j.
@@ -349,7 +372,7 @@ __device__ __forceinline__ void run_batch(const WarpQueue& q, int n, const doubl
                                           double* __restrict__ out_xyz) {
   const int lane = threadIdx.x & 31;
   const sgi::SmemIn2 in = {smem_u32(&q.v[0][lane][0]), (uint32_t)sizeof(q.v[0])};
-  const sgi::W2 zz = in(6);
+  const sgi::W2 zz = {tab[q.lat[lane]], tab[q.lat[lane + 32]]};
   auto store = [&](const sgi::QueryOut& o, double z0, bool ok, int r) {
     if (r >= n) return;
     const int64_t j = q.slot[r];
@@ -367,7 +390,7 @@ __device__ __forceinline__ void run_batch(const WarpQueue& q, int n, const doubl
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const sgi::SmemIn in1 = {smem_u32(&q.v[0][lane][h]), (uint32_t)sizeof(q.v[0])};
-      const double z0 = in1(6);
+      const double z0 = h ? zz.y : zz.x;
       sgi::QueryOut o;
       const bool ok = sgi::query_fast<MODE>(in1, z0, o);
       store(o, z0, ok, lane + 32 * h);
@@ -404,33 +427,47 @@ sgi_zonal_emit_warp_kernel(const double* __restrict__ va, const double* __restri
   auto seg_edge0 = [&](int g) {
     return (t0 + (int64_t)(g / kSegs) * nwarps) * kEdges + (g % kSegs) * kSegEdges;
   };
-  auto load_cand = [&](int g, int4& a, int4& b) {      // lane's four (klo, kcnt), 0 beyond ne
-    a = make_int4(0, 0, 0, 0);
-    b = a;
-    if (g >= nseg) return;
-    const int64_t e = seg_edge0(g) + l0;
-    if (e + 3 < ne) {
-      a = __ldg(reinterpret_cast<const int4*>(cand + e));
-      b = __ldg(reinterpret_cast<const int4*>(cand + e + 2));
-    } else {
-      if (e < ne) { const int2 c = cand[e]; a.x = c.x; a.y = c.y; }
-      if (e + 1 < ne) { const int2 c = cand[e + 1]; a.z = c.x; a.w = c.y; }
-      if (e + 2 < ne) { const int2 c = cand[e + 2]; b.x = c.x; b.y = c.y; }
+  // candidate ranges of segment g -> ring slot g % kCandRing by one bulk copy (lane 0), so the
+  // next kCandRing - 1 segments are in flight without holding registers
+  if (lane == 0) {
+    for (int r = 0; r < kCandRing; ++r) mbar_init(&W.full[r], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  auto issue = [&](int g) {
+    if (lane != 0 || g >= nseg) return;
+    const int64_t e0 = seg_edge0(g);
+    const int64_t nv = ne - e0 < kSegEdges ? ne - e0 : kSegEdges;
+    if (nv <= 0) {                                     // past the last edge: complete the phase
+      mbar_expect_tx(&W.full[g % kCandRing], 0);
+      return;
     }
+    // whole 16-B units (an odd count reads 8 B of the tile sums that follow cand in d_work)
+    const uint32_t bytes = (uint32_t)((nv + 1) / 2 * 16);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&W.full[g % kCandRing], bytes);
+    bulk_g2s(&W.cand[g % kCandRing][0], cand + e0, bytes, &W.full[g % kCandRing]);
   };
-  int4 na, nb;
-  load_cand(0, na, nb);
+  for (int g = 0; g < kCandRing - 1; ++g) issue(g);
   unsigned long long nbase = nseg > 0 ? tile_base[t0] : 0;
   int cur = 0, qn = 0;                                 // filling queue, its queued pairs
   bool pending = false;                                // queue cur ^ 1 gathered, not yet run
   int64_t base = 0;                                    // first slot of the current segment
   for (int g = 0; g < nseg; ++g) {
-    const int4 ca = na, cb = nb;
+    issue(g + kCandRing - 1);
     const int64_t e0 = seg_edge0(g);
     if (g % kSegs == 0) base = (int64_t)nbase;
-    load_cand(g + 1, na, nb);                          // prefetch the next segment
     if ((g + 1) % kSegs == 0 && g + 1 < nseg)
       nbase = tile_base[t0 + (int64_t)((g + 1) / kSegs) * nwarps];
+    mbar_wait(&W.full[g % kCandRing], (uint32_t)((g / kCandRing) & 1));
+    int4 ca = *reinterpret_cast<const int4*>(&W.cand[g % kCandRing][l0]);
+    int4 cb = *reinterpret_cast<const int4*>(&W.cand[g % kCandRing][l0 + 2]);
+    if (e0 + l0 + 3 >= ne) {                           // entries beyond ne: no candidates
+      if (e0 + l0 >= ne) ca.y = 0;
+      if (e0 + l0 + 1 >= ne) ca.w = 0;
+      if (e0 + l0 + 2 >= ne) cb.y = 0;
+      cb.w = 0;
+    }
     const unsigned k0 = (unsigned)ca.y, k1 = (unsigned)ca.w, k2 = (unsigned)cb.y;
     const unsigned mine = k0 + k1 + k2 + (unsigned)cb.w;
     unsigned incl = mine;
@@ -475,7 +512,6 @@ sgi_zonal_emit_warp_kernel(const double* __restrict__ va, const double* __restri
             cp_async8(&q.v[c][lane][h], va + c * lde + e);
             cp_async8(&q.v[3 + c][lane][h], vb + c * lde + e);
           }
-          q.v[6][lane][h] = tab[k];
           q.edge[at] = e;
           q.lat[at] = k;
           q.slot[at] = base + p;
@@ -496,6 +532,7 @@ sgi_zonal_emit_warp_kernel(const double* __restrict__ va, const double* __restri
       }
     }
     base += segtot;
+    __syncwarp();                                      // ring slot g % kCandRing is reissued next
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
   asm volatile("cp.async.wait_all;" ::: "memory");

@@ -14,7 +14,8 @@ sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "build", "zvariants")
 VARIANTS = {
     "emit_t256": {},
-    "emit_t512": {"SGI_ZONAL_WTHREADS": 512},
+    "f_minb4": {"SGI_ZONAL_FILTER_MINB": 4},
+    "f_pf_minb2": {"SGI_ZONAL_FILTER_PREFETCH": 1, "SGI_ZONAL_FILTER_MINB": 2},
 }
 
 
