@@ -97,8 +97,8 @@ sgi_status sgi_count_histogram(const uint8_t* out_count, int64_t n,
  * vb[c*ld_e + e] (device); lat_z0[n_lat] is strictly increasing (device).  For each edge, the
  * candidate latitudes are those within delta = 2^-40 of the arc's z-range (endpoint heights
  * z/|x| and, when the great circle's extremum lies inside the arc, the apex height
- * sqrt(|n_xy|^2/|n|^2), from the EFT normal); an edge with n = 0 (degenerate at every
- * latitude) has every latitude as a candidate.  Every (edge, latitude) whose query has a
+ * sqrt(|n_xy|^2/|n|^2), from a normal accurate to 2 ulps per component); an edge with n = 0
+ * (degenerate at every latitude) has every latitude as a candidate.  Every (edge, latitude) whose query has a
  * nonzero count is a candidate; candidates within delta of the range may have count 0.
  * Candidate pair j (edge-major, latitude ascending; deterministic) is written to out_edge[j],
  * out_lat[j], out_count[j] and out_xyz[(slot*3 + c)*cap + j], bit-identical to

@@ -2,7 +2,7 @@
 // (the paper's motivating application, zonal means on regridding meshes).
 //
 // Three launches over tiles of kEdges consecutive edges:
-//   filter per edge, from the accurate (AccuDOP) normal rounded once, the arc's z-range: the
+//   filter per edge, from an accurate normal (each component within 2 ulps), the arc's z-range: the
 //          endpoints' z/|x| and, when the great circle's extremum lies strictly inside the arc
 //          (dz/dt changes sign: g1 = (n x a)_z > 0 > g2 = (n x b)_z for a maximum), the apex
 //          height sqrt(|n_xy|^2/|n|^2); widened by delta = 2^-40 (far above its rounding error);
@@ -114,19 +114,27 @@ __device__ __forceinline__ double fast_rsqrt(double x) {
   return y;
 }
 
+// a*b - c*d within 2 ulps of the exact value (Kahan's difference of products with FMA: w = RN(cd),
+// e = w - cd exactly, result RN(RN(ab - w) + e)) — the filter's normal, accurate in direction
+// for any arc length, in 4 operations and a 3-deep chain.
+__device__ __forceinline__ double kahan_dop(double a, double b, double c, double d) {
+  const double w = __dmul_rn(c, d);
+  const double e = __fma_rn(-c, d, w);
+  const double f = __fma_rn(a, b, -w);
+  return __dadd_rn(f, e);
+}
+
 // Candidate latitudes [klo, klo + kcnt) of one edge (see the file comment).  The filter needs the
-// direction of n only to a few ulps: it takes the renormalised EFT normal's high parts (RN of the
-// exact n, so short arcs keep their accuracy) and evaluates heights with the device rsqrt (a few
-// ulps, deterministic) — errors ~1e-15, far below delta.
+// direction of n only to a few ulps: each component within 2 ulps of the exact one (kahan_dop, so
+// short arcs keep their accuracy) and heights from the device rsqrt (a few ulps, deterministic) —
+// errors ~1e-15, far below delta.
 __device__ __forceinline__ void candidates(const double* x, const double* tab, const int* bkt,
                                            int nlat, int& klo, int& kcnt) {
   klo = 0;
   kcnt = 0;
-  const sgi::dd nxp = sgi::accu_dop(x[1], x[5], x[2], x[4]);
-  const sgi::dd nyp = sgi::accu_dop(x[2], x[3], x[0], x[5]);
-  const sgi::dd nzp = sgi::accu_dop(x[0], x[4], x[1], x[3]);
-  const double nx = __dadd_rn(nxp.hi, nxp.lo), ny = __dadd_rn(nyp.hi, nyp.lo);
-  const double nz = __dadd_rn(nzp.hi, nzp.lo);
+  const double nx = kahan_dop(x[1], x[5], x[2], x[4]);
+  const double ny = kahan_dop(x[2], x[3], x[0], x[5]);
+  const double nz = kahan_dop(x[0], x[4], x[1], x[3]);
   const double ra2 = __dadd_rn(__dadd_rn(__dmul_rn(x[0], x[0]), __dmul_rn(x[1], x[1])), __dmul_rn(x[2], x[2]));
   const double rb2 = __dadd_rn(__dadd_rn(__dmul_rn(x[3], x[3]), __dmul_rn(x[4], x[4])), __dmul_rn(x[5], x[5]));
   const double za = __dmul_rn(x[2], fast_rsqrt(ra2)), zb = __dmul_rn(x[5], fast_rsqrt(rb2));
