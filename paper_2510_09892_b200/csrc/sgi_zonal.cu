@@ -37,8 +37,7 @@ namespace {
 #define SGI_ZONAL_THREADS 256
 #endif
 #ifndef SGI_ZONAL_FILTER_PREFETCH
-#define SGI_ZONAL_FILTER_PREFETCH 0   // 1: the next tile's edges load into registers during this
-                                      // one (110 regs, 2 CTAs/SM; 3 CTAs/SM without: 0.480 vs 0.483 ms)
+#define SGI_ZONAL_FILTER_PREFETCH 0   // next tile's edges: 0 none, 1 registers, 2 cp.async to smem
 #endif
 #ifndef SGI_ZONAL_FILTER_MINB
 #define SGI_ZONAL_FILTER_MINB 3     // 80 regs: 24 warps/SM (the filter is latency-bound)
@@ -90,6 +89,11 @@ __device__ __forceinline__ int bucket_search(const int* bkt, const double* tab, 
   const int lo = b >= 1 ? bkt[b - 1] : 0;
   const int hi = b + 2 <= kBuckets - 1 ? bkt[b + 2] : nlat;
   return lo + (UPPER ? upper_bound(tab + lo, hi - lo, x) : lower_bound(tab + lo, hi - lo, x));
+}
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
 }
 
 struct EdgeX {
@@ -188,19 +192,10 @@ sgi_zonal_filter_kernel(const double* __restrict__ va, const double* __restrict_
   build_buckets(s_bkt, tab, nlat);
   const int64_t ntiles = (ne + kEdges - 1) / kEdges;
   const int64_t G = gridDim.x;
-  // tile t: candidates of the thread's two edges from `cur` while the edges of tile t + G load
-  // into `nxt`; per-warp sums (32-bit: <= 64 x 2^23) meet in s_red[parity] behind one barrier
-  auto step = [&](int64_t t, int parity, EdgeX (&cur)[2], EdgeX (&nxt)[2]) {
-    const int64_t e0 = t * kEdges + 2 * threadIdx.x, en = e0 + G * kEdges;
-#if SGI_ZONAL_FILTER_PREFETCH
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-      if (en + j < ne) load_edge(nxt[j], va, vb, lde, en + j);
-#else
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-      if (e0 + j < ne) load_edge(cur[j], va, vb, lde, e0 + j);
-#endif
+  // candidates of the thread's two edges of tile t; per-warp sums (32-bit: <= 64 x 2^23) meet in
+  // s_red[parity] behind one barrier, which also keeps the warps within one tile of each other
+  auto finish = [&](int64_t t, int parity, const EdgeX (&cur)[2]) {
+    const int64_t e0 = t * kEdges + 2 * threadIdx.x;
     unsigned sum = 0;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
@@ -214,7 +209,7 @@ sgi_zonal_filter_kernel(const double* __restrict__ va, const double* __restrict_
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, d);
     if ((threadIdx.x & 31) == 0) s_red[parity][threadIdx.x >> 5] = sum;
-    __syncthreads();        // also keeps warps within one tile, so s_red[parity] is free again
+    __syncthreads();
     if (threadIdx.x == 0) {
       unsigned long long acc = 0;
 #pragma unroll
@@ -222,7 +217,51 @@ sgi_zonal_filter_kernel(const double* __restrict__ va, const double* __restrict_
       tile_sum[t] = acc;
     }
   };
-  EdgeX A[2], B[2];                                    // ping-pong: no register copies
+#if SGI_ZONAL_FILTER_PREFETCH == 2
+  // the next tile's endpoints by cp.async into a shared double buffer (each thread copies and
+  // later reads only its own two edges, so no barrier guards the buffer)
+  double* stage = s_lat + (SMEM ? ((size_t)nlat + 1) / 2 * 2 : 0);
+  auto slot = [&](int buf, int c, int l) { return stage + ((size_t)buf * 6 + c) * kEdges + l; };
+  auto issue = [&](int64_t t, int buf) {
+    if (t < ntiles) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int l = 2 * threadIdx.x + j;
+        const int64_t e = t * kEdges + l;
+        if (e < ne) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            cp_async8(slot(buf, c, l), va + c * lde + e);
+            cp_async8(slot(buf, 3 + c, l), vb + c * lde + e);
+          }
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  issue(blockIdx.x, 0);
+  int buf = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += G, buf ^= 1) {
+    issue(t + G, buf ^ 1);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    EdgeX cur[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int c = 0; c < 6; ++c) cur[j].x[c] = *slot(buf, c, 2 * threadIdx.x + j);
+    finish(t, buf, cur);
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+#elif SGI_ZONAL_FILTER_PREFETCH == 1
+  // the next tile's edges load into registers during this one (ping-pong, no register copies)
+  EdgeX A[2], B[2];
+  auto step = [&](int64_t t, int parity, EdgeX (&cur)[2], EdgeX (&nxt)[2]) {
+    const int64_t en = t * kEdges + 2 * threadIdx.x + G * kEdges;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      if (en + j < ne) load_edge(nxt[j], va, vb, lde, en + j);
+    finish(t, parity, cur);
+  };
   int64_t t = blockIdx.x;
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
@@ -233,6 +272,18 @@ sgi_zonal_filter_kernel(const double* __restrict__ va, const double* __restrict_
     step(t, 0, A, B);
     if (t + G < ntiles) step(t + G, 1, B, A);
   }
+#else
+  int parity = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += G, parity ^= 1) {
+    EdgeX cur[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int64_t e = t * kEdges + 2 * threadIdx.x + j;
+      if (e < ne) load_edge(cur[j], va, vb, lde, e);
+    }
+    finish(t, parity, cur);
+  }
+#endif
 }
 
 // Pass 2: exclusive scan of the tile sums in place, the total to *d_total (one CTA).  Rounds of
@@ -294,11 +345,6 @@ sgi_zonal_scan_kernel(unsigned long long* __restrict__ tile_sum, int64_t ntiles,
     __syncthreads();
   }
   if (tid == 0) *d_total = carry;
-}
-
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src)
-               : "memory");
 }
 
 // Pair j of the output: (edge, k), its count and both slots (unused slots: canonical NaN).
@@ -605,7 +651,8 @@ sgi_status sgi_zonal_intersect(const double* va, const double* vb, int64_t n_edg
     return (int)(g < ntiles ? g : ntiles);
   };
   const bool smem_tab = n_lat <= kLatSmem;
-  const size_t filter_smem = lat_smem;
+  const size_t filter_smem = (SGI_ZONAL_FILTER_PREFETCH == 2 ? lat_smem_even : lat_smem) +
+                             (SGI_ZONAL_FILTER_PREFETCH == 2 ? 2 * 6 * kEdges * sizeof(double) : 0);
   if (smem_tab) {
     const int gf = grid_for(sgi_zonal_filter_kernel<true>, filter_smem);
     sgi_zonal_filter_kernel<true><<<gf, kThreads, filter_smem, st>>>(va, vb, n_edges, ld_e, lat_z0,

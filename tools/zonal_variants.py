@@ -1,7 +1,8 @@
 """Build and time launch-shape variants of the fused zonal pass (tools, not product).
     python tools/zonal_variants.py build      # here
     python tools/zonal_variants.py time       # on the GPU: C4 mesh x 1,800 latitudes
-Knobs: SGI_ZONAL_THREADS (tile = 2x edges), SGI_ZONAL_FUSE, SGI_ZONAL_WTHREADS (emit CTA size)."""
+Knobs: SGI_ZONAL_THREADS (tile = 2x edges), SGI_ZONAL_FILTER_MINB, SGI_ZONAL_FILTER_PREFETCH (0/1/2),
+SGI_ZONAL_WTHREADS (emit CTA size)."""
 import ctypes
 import json
 import os
@@ -15,7 +16,9 @@ OUT = os.path.join(ROOT, "build", "zvariants")
 VARIANTS = {
     "emit_t256": {},
     "f_minb4": {"SGI_ZONAL_FILTER_MINB": 4},
-    "f_pf_minb2": {"SGI_ZONAL_FILTER_PREFETCH": 1, "SGI_ZONAL_FILTER_MINB": 2},
+    "f_minb5": {"SGI_ZONAL_FILTER_MINB": 5},
+    "f_minb6": {"SGI_ZONAL_FILTER_MINB": 6},
+    "t512": {"SGI_ZONAL_THREADS": 512, "SGI_ZONAL_FILTER_MINB": 2},
 }
 
 
