@@ -381,11 +381,16 @@ __device__ __forceinline__ void store_pair(const sgi::QueryOut& o, double z0, in
 #ifndef SGI_ZONAL_WTHREADS
 #define SGI_ZONAL_WTHREADS 256   // 2 CTAs per SM (0.489 ms per C4 pass vs 0.496 at 512)
 #endif
-constexpr int kWThreads = SGI_ZONAL_WTHREADS, kWarpsPerCta = kWThreads / 32, kBatch = 64;
+#ifndef SGI_ZONAL_EMIT_W2
+#define SGI_ZONAL_EMIT_W2 1        // 1: two queries per lane (W2); 0: one per lane, more warps
+#endif
+constexpr int kHalves = SGI_ZONAL_EMIT_W2 ? 2 : 1;
+constexpr int kWThreads = SGI_ZONAL_WTHREADS, kWarpsPerCta = kWThreads / 32, kBatch = 32 * kHalves;
+constexpr int kEmitMinB = (SGI_ZONAL_EMIT_W2 ? 512 : 768) / kWThreads;
 constexpr int kSegEdges = 128;
 static_assert(kEdges % kSegEdges == 0, "a tile is a whole number of segments");
 struct alignas(16) WarpQueue {
-  double v[6][32][2];              // planes a_x .. b_z; [column][half]
+  double v[6][32][kHalves];        // planes a_x .. b_z; [column][half]
   long long edge[kBatch];
   long long slot[kBatch];
   int lat[kBatch];
@@ -425,8 +430,6 @@ __device__ __forceinline__ void run_batch(const WarpQueue& q, int n, const doubl
                                           uint8_t* __restrict__ out_count,
                                           double* __restrict__ out_xyz) {
   const int lane = threadIdx.x & 31;
-  const sgi::SmemIn2 in = {smem_u32(&q.v[0][lane][0]), (uint32_t)sizeof(q.v[0])};
-  const sgi::W2 zz = {tab[q.lat[lane]], tab[q.lat[lane + 32]]};
   auto store = [&](const sgi::QueryOut& o, double z0, bool ok, int r) {
     if (r >= n) return;
     const int64_t j = q.slot[r];
@@ -435,16 +438,18 @@ __device__ __forceinline__ void run_batch(const WarpQueue& q, int n, const doubl
     else emit_exact<MODE>(va, vb, lde, tab, q.edge[r], q.lat[r], j, cap, out_edge, out_lat,
                           out_count, out_xyz);
   };
-  if constexpr (MODE == sgi::MODE_EFT || MODE == sgi::MODE_EFT_LITERAL) {
+  if constexpr (kHalves == 2 && (MODE == sgi::MODE_EFT || MODE == sgi::MODE_EFT_LITERAL)) {
+    const sgi::SmemIn2 in = {smem_u32(&q.v[0][lane][0]), (uint32_t)sizeof(q.v[0])};
+    const sgi::W2 zz = {tab[q.lat[lane]], tab[q.lat[lane + 32]]};
     sgi::QueryOut2 o;
     const sgi::B2 ok = sgi::query_fast2<MODE>(in, zz, o);
     store({o.p0x.x, o.p0y.x, o.p1x.x, o.p1y.x, o.count[0]}, zz.x, ok.x, lane);
     store({o.p0x.y, o.p0y.y, o.p1x.y, o.p1y.y, o.count[1]}, zz.y, ok.y, lane + 32);
   } else {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < kHalves; ++h) {
       const sgi::SmemIn in1 = {smem_u32(&q.v[0][lane][h]), (uint32_t)sizeof(q.v[0])};
-      const double z0 = h ? zz.y : zz.x;
+      const double z0 = tab[q.lat[lane + 32 * h]];
       sgi::QueryOut o;
       const bool ok = sgi::query_fast<MODE>(in1, z0, o);
       store(o, z0, ok, lane + 32 * h);
@@ -453,7 +458,7 @@ __device__ __forceinline__ void run_batch(const WarpQueue& q, int n, const doubl
 }
 
 template <int MODE, bool SMEM>
-__global__ void __launch_bounds__(kWThreads, 512 / kWThreads)
+__global__ void __launch_bounds__(kWThreads, kEmitMinB)
 sgi_zonal_emit_warp_kernel(const double* __restrict__ va, const double* __restrict__ vb,
                            int64_t ne, int64_t lde, const double* __restrict__ lat, int nlat,
                            int64_t cap, int64_t* __restrict__ out_edge,
@@ -538,7 +543,7 @@ sgi_zonal_emit_warp_kernel(const double* __restrict__ va, const double* __restri
       // slot-major fill: lane L fills slots L and L + 32; pair p's owner lane is the last lane
       // with excl <= p (found by a shuffle binary search), then one of its four edges
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < kHalves; ++h) {
         const int at = lane + 32 * h;
         const bool valid = at >= qn && at < qn + (int)m;
         const unsigned p = min(cursor + (unsigned)(at - qn), segtot - 1);   // clamped when idle

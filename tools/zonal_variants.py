@@ -15,10 +15,7 @@ sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "build", "zvariants")
 VARIANTS = {
     "emit_t256": {},
-    "f_minb4": {"SGI_ZONAL_FILTER_MINB": 4},
-    "f_minb5": {"SGI_ZONAL_FILTER_MINB": 5},
-    "f_minb6": {"SGI_ZONAL_FILTER_MINB": 6},
-    "t512": {"SGI_ZONAL_THREADS": 512, "SGI_ZONAL_FILTER_MINB": 2},
+    "emit_scalar": {"SGI_ZONAL_EMIT_W2": 0},
 }
 
 
