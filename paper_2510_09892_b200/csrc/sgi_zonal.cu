@@ -457,6 +457,17 @@ __device__ __forceinline__ void run_batch(const WarpQueue& q, int n, const doubl
   }
 }
 
+template <int MODE>
+__device__ __noinline__ void run_batch_tail(const WarpQueue& q, int n, const double* tab,
+                                            const double* __restrict__ va,
+                                            const double* __restrict__ vb, int64_t lde,
+                                            int64_t cap, int64_t* __restrict__ out_edge,
+                                            int32_t* __restrict__ out_lat,
+                                            uint8_t* __restrict__ out_count,
+                                            double* __restrict__ out_xyz) {
+  run_batch<MODE>(q, n, tab, va, vb, lde, cap, out_edge, out_lat, out_count, out_xyz);
+}
+
 template <int MODE, bool SMEM>
 __global__ void __launch_bounds__(kWThreads, kEmitMinB)
 sgi_zonal_emit_warp_kernel(const double* __restrict__ va, const double* __restrict__ vb,
@@ -595,10 +606,12 @@ sgi_zonal_emit_warp_kernel(const double* __restrict__ va, const double* __restri
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
   asm volatile("cp.async.wait_all;" ::: "memory");
+  // the last one or two queues: one out-of-line copy of the batch code (instruction cache)
   if (pending)
-    run_batch<MODE>(W.q[cur ^ 1], kBatch, tab, va, vb, lde, cap, out_edge, out_lat, out_count,
-                    out_xyz);
-  if (qn > 0) run_batch<MODE>(W.q[cur], qn, tab, va, vb, lde, cap, out_edge, out_lat, out_count, out_xyz);
+    run_batch_tail<MODE>(W.q[cur ^ 1], kBatch, tab, va, vb, lde, cap, out_edge, out_lat, out_count,
+                         out_xyz);
+  if (qn > 0)
+    run_batch_tail<MODE>(W.q[cur], qn, tab, va, vb, lde, cap, out_edge, out_lat, out_count, out_xyz);
 }
 
 }  // namespace
