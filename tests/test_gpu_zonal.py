@@ -148,3 +148,32 @@ def test_c4_full_size_against_unfused_path():
     assert np.array_equal(res["count"][jf], cnt[ju])
     assert same(res["xyz"][:, :, jf], out[:, :, ju]).all()
     assert total >= len(nz_unfused) and len(nz_unfused) > 5_900_000
+
+
+@pytest.mark.parametrize("pad,shift", [(5, 1), (0, 1), (37, 0)])
+def test_padded_and_unaligned_edge_planes(pad, shift):
+    """Edge planes with ld_e > n_edges and a base only 8-byte aligned (a view one element into a
+    buffer): same pairs and values as the packed call; the workspace stays 16-byte aligned."""
+    a, b, _ = sgi_inputs.generate_host(2, 3001)
+    lat = sgi_inputs.latitudes(500)
+    ref, t_ref = run_zonal(a, b, lat)
+    n = a.shape[1]
+    ld = n + pad
+    dl = torch.from_numpy(lat).cuda()
+
+    def planes(x):
+        buf = torch.full((3 * ld + shift,), float("nan"), dtype=torch.float64, device="cuda")
+        v = buf[shift:].view(3, ld)
+        v[:, :n] = torch.from_numpy(x).cuda()
+        return v
+
+    va, vb = planes(a), planes(b)
+    assert va.data_ptr() % 16 == 8 * shift % 16
+    out = sgi.zonal_intersect(va, vb, dl, mode="eft", n_edges=n)
+    torch.cuda.synchronize()
+    m = int(out["total"].item())
+    assert m == t_ref
+    assert np.array_equal(out["edge"][:m].cpu().numpy(), ref["edge"])
+    assert np.array_equal(out["lat"][:m].cpu().numpy(), ref["lat"])
+    assert np.array_equal(out["count"][:m].cpu().numpy(), ref["count"])
+    assert same(out["xyz"][..., :m].cpu().numpy(), ref["xyz"]).all()
