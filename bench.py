@@ -449,7 +449,10 @@ def main():
         e2e = {"value": n_total / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": n_total * 56, "d2h_bytes_per_step": n_total * 49,
                "steps": args.e2e_steps, "path": "sgi_intersect_arc_lat_host (pinned host buffers)",
-               "link_gbs_measured": link, "link_frac": (n * 105 / e2e_s / 1e9) / link}
+               "link_gbs_measured": link, "link_frac": (n * 105 / e2e_s / 1e9) / link,
+               # each direction gets ~link/2 when both run; the 56-B H2D side binds
+               "link_bound_queries_per_s": link / 2 * 1e9 / 56,
+               "link_bound_frac": (n / e2e_s) / (link / 2 * 1e9 / 56)}
         del ha, hb, hz, hout, hcnt, work
 
     cpu = None
