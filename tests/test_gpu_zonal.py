@@ -86,7 +86,9 @@ def test_small_mesh_against_brute_force():
 
 
 @pytest.mark.parametrize("mode,omode", [("eft", oracle.MODE_EFT), ("eft_literal", oracle.MODE_EFT_LITERAL),
-                                        ("naive", oracle.MODE_NAIVE)])
+                                        ("naive", oracle.MODE_NAIVE), ("yac", oracle.MODE_YAC),
+                                        ("base", oracle.MODE_BASE),
+                                        ("naive_kahan", oracle.MODE_NAIVE_KAHAN)])
 def test_long_arcs_many_latitudes(mode, omode):
     """C1 arcs (long, up to pi) against 181 latitudes: edges spanning many latitudes, two-point
     pairs, dense redistribution of candidates across threads."""
