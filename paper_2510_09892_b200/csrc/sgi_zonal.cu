@@ -40,7 +40,7 @@ namespace {
 #define SGI_ZONAL_FILTER_PREFETCH 0   // next tile's edges: 0 none, 1 registers, 2 cp.async to smem
 #endif
 #ifndef SGI_ZONAL_FILTER_MINB
-#define SGI_ZONAL_FILTER_MINB 3     // 80 regs: 24 warps/SM (the filter is latency-bound)
+#define SGI_ZONAL_FILTER_MINB 3     // <= 80 regs (64 used: 4 CTAs, 32 warps/SM; latency-bound)
 #endif
 constexpr int kThreads = SGI_ZONAL_THREADS;       // threads per CTA
 constexpr int kEdges = 2 * kThreads;              // edges per tile (two adjacent per thread)

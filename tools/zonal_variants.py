@@ -2,7 +2,7 @@
     python tools/zonal_variants.py build      # here
     python tools/zonal_variants.py time       # on the GPU: C4 mesh x 1,800 latitudes
 Knobs: SGI_ZONAL_THREADS (tile = 2x edges), SGI_ZONAL_FILTER_MINB, SGI_ZONAL_FILTER_PREFETCH (0/1/2),
-SGI_ZONAL_WTHREADS (emit CTA size)."""
+SGI_ZONAL_WTHREADS (emit CTA size), SGI_ZONAL_EMIT_W2 (two queries per lane)."""
 import ctypes
 import json
 import os
