@@ -381,6 +381,9 @@ __device__ __forceinline__ void store_pair(const sgi::QueryOut& o, double z0, in
 #ifndef SGI_ZONAL_WTHREADS
 #define SGI_ZONAL_WTHREADS 256   // 2 CTAs per SM (0.489 ms per C4 pass vs 0.496 at 512)
 #endif
+#ifndef SGI_ZONAL_EMIT_REVERSE
+#define SGI_ZONAL_EMIT_REVERSE 1   // emit tiles in the reverse of the filter's order (L2 reuse)
+#endif
 #ifndef SGI_ZONAL_EMIT_W2
 #define SGI_ZONAL_EMIT_W2 1        // 1: two queries per lane (W2); 0: one per lane, more warps
 #endif
@@ -494,8 +497,14 @@ sgi_zonal_emit_warp_kernel(const double* __restrict__ va, const double* __restri
   constexpr int kSegs = kEdges / kSegEdges;
   const int nseg = mytiles * kSegs;                    // this warp's segments, in order
   const int l0 = 4 * lane;
+  // this warp's i-th tile; in reverse order the first tiles are the filter's last ones, whose
+  // endpoints and candidate ranges are still in L2
+  auto tile_of = [&](int i) {
+    const int64_t t = t0 + (int64_t)i * nwarps;
+    return SGI_ZONAL_EMIT_REVERSE ? ntiles - 1 - t : t;
+  };
   auto seg_edge0 = [&](int g) {
-    return (t0 + (int64_t)(g / kSegs) * nwarps) * kEdges + (g % kSegs) * kSegEdges;
+    return tile_of(g / kSegs) * kEdges + (g % kSegs) * kSegEdges;
   };
   // candidate ranges of segment g -> ring slot g % kCandRing by one bulk copy (lane 0), so the
   // next kCandRing - 1 segments are in flight without holding registers
@@ -519,7 +528,7 @@ sgi_zonal_emit_warp_kernel(const double* __restrict__ va, const double* __restri
     bulk_g2s(&W.cand[g % kCandRing][0], cand + e0, bytes, &W.full[g % kCandRing]);
   };
   for (int g = 0; g < kCandRing - 1; ++g) issue(g);
-  unsigned long long nbase = nseg > 0 ? tile_base[t0] : 0;
+  unsigned long long nbase = nseg > 0 ? tile_base[tile_of(0)] : 0;
   int cur = 0, qn = 0;                                 // filling queue, its queued pairs
   bool pending = false;                                // queue cur ^ 1 gathered, not yet run
   int64_t base = 0;                                    // first slot of the current segment
@@ -528,7 +537,7 @@ sgi_zonal_emit_warp_kernel(const double* __restrict__ va, const double* __restri
     const int64_t e0 = seg_edge0(g);
     if (g % kSegs == 0) base = (int64_t)nbase;
     if ((g + 1) % kSegs == 0 && g + 1 < nseg)
-      nbase = tile_base[t0 + (int64_t)((g + 1) / kSegs) * nwarps];
+      nbase = tile_base[tile_of((g + 1) / kSegs)];
     mbar_wait(&W.full[g % kCandRing], (uint32_t)((g / kCandRing) & 1));
     int4 ca = *reinterpret_cast<const int4*>(&W.cand[g % kCandRing][l0]);
     int4 cb = *reinterpret_cast<const int4*>(&W.cand[g % kCandRing][l0 + 2]);

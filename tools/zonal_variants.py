@@ -15,7 +15,7 @@ sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "build", "zvariants")
 VARIANTS = {
     "emit_t256": {},
-    "emit_scalar": {"SGI_ZONAL_EMIT_W2": 0},
+    "forward": {"SGI_ZONAL_EMIT_REVERSE": 0},
 }
 
 
