@@ -58,7 +58,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--workload", default="arcs", choices=["arcs", "zonal"],
+    p.add_argument("--workload", default="arcs", choices=["arcs", "zonal", "dw", "trace"],
                    help="arcs: the C2/C3/C5 batch (default line); zonal: the fused zonal-mean "
                         "pass over the C4 cubed sphere (ne=1024) x 1,800 latitudes")
     return p.parse_args()
@@ -316,12 +316,86 @@ def run_zonal(args):
     print(json.dumps(line), flush=True)
 
 
+EFT_OPS = 362          # algorithmic FP64 ops per query of SGI_MODE_EFT
+DW_EXTRA_OPS = 28      # per query: 4 low parts x (fma, 4 add/sub, 1 mul, 1 division), include/sgi.h
+TRACE_FIELDS = 38
+
+
+def run_extra(args):
+    """SURVEY §8(f4) paths on the default workload (C2, 2^24 arcs, one GPU): `dw` =
+    sgi_intersect_arc_lat_dw (double-word points), `trace` = sgi_intersect_trace (the 38
+    Appendix-A intermediates per query).  Device-resident inputs and outputs, one launch per
+    step, CUDA events on the launching stream."""
+    import ctypes
+    import torch
+    import paper_2510_09892_b200 as sgi
+    import sgi_inputs
+    dev = torch.device("cuda", 0)
+    n, cfg, mode = args.n, args.config, args.mode
+    a = torch.empty((3, n), dtype=torch.float64, device=dev)
+    b = torch.empty_like(a)
+    z0 = torch.empty(n, dtype=torch.float64, device=dev)
+    sgi_inputs.generate_device(cfg, n, a, b, z0, seed=SEEDS[cfg])
+    cnt = torch.empty(n, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    L = sgi._load()
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    mcode = sgi._mode(mode)
+    if args.workload == "dw":
+        out = torch.empty((2, 3, n), dtype=torch.float64, device=dev)
+        lo = torch.empty((2, 2, n), dtype=torch.float64, device=dev)
+
+        def step():
+            rc = L.sgi_intersect_arc_lat_dw(a.data_ptr(), b.data_ptr(), z0.data_ptr(), n, n,
+                                            out.data_ptr(), lo.data_ptr(), cnt.data_ptr(), mcode, sp)
+            assert rc == 0, rc
+        byts, ops = 56 + 48 + 32 + 1, EFT_OPS + DW_EXTRA_OPS
+        what = "sgi_intersect_arc_lat_dw (double-word points, reading R11)"
+    else:
+        trace = torch.empty((TRACE_FIELDS, n), dtype=torch.float64, device=dev)
+
+        def step():
+            rc = L.sgi_intersect_trace(a.data_ptr(), b.data_ptr(), z0.data_ptr(), n, n,
+                                       trace.data_ptr(), cnt.data_ptr(), mcode, sp)
+            assert rc == 0, rc
+        byts, ops = 56 + 8 * TRACE_FIELDS + 1, EFT_OPS
+        what = "sgi_intersect_trace (38 Appendix-A intermediates per query)"
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clocks:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    s = e0.elapsed_time(e1) * 1e-3 / args.steps
+    peaks = load_peaks()
+    alu_peak = 148 * 64 * peaks["sm_max_mhz"] * 1e6 / 1e12
+    alu_frac = n * ops / s / 1e12 / alu_peak
+    hbm_frac = n * byts / s / 1e9 / peaks["hbm_gbs"]
+    line = {"metric": f"{args.workload} queries/s", "value": n / s, "unit": "queries/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": s * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": CONFIG_DESC[cfg], "mode": mode, "queries": n, "path": what,
+                       "bytes_per_query": byts, "fp64_ops_per_query": ops},
+            "roofline": {"bound": "alu" if alu_frac > hbm_frac else "hbm",
+                         "alu_frac": alu_frac, "hbm_frac": hbm_frac,
+                         "peak_alu": alu_peak, "peak_hbm": peaks["hbm_gbs"]},
+            "clocks": clocks.summary(), "gpu_launches": args.steps}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
     if args.workload == "zonal":
         return run_zonal(args)
+    if args.workload in ("dw", "trace"):
+        return run_extra(args)
 
     import torch
     import torch.distributed as dist
