@@ -344,10 +344,12 @@ def test_output_stats_kernel():
 
 
 # ------------------------------------------------------- double-word points (§8(f4), R11)
-@pytest.mark.parametrize("config,n", [(1, 10_000), (3, 30_000), (6, 17 * 1000), (7, 13 * 1000)])
+@pytest.mark.parametrize("config,n", [(1, 10_000), (3, 30_000), (6, 17 * 1000), (7, 13 * 1000),
+                                      (2, (1 << 19) + 333), (3, (1 << 19) + 1000)])
 @pytest.mark.parametrize("mode,omode", [("eft", oracle.MODE_EFT),
                                         ("eft_literal", oracle.MODE_EFT_LITERAL)])
 def test_double_word_parity(config, n, mode, omode):
+    """Small batches run the grid-stride kernel, n >= 2^19 the TMA-staged one (with a tail)."""
     a, b, z0 = sgi_inputs.generate_host(config, n)
     da, db, dz = (torch.from_numpy(x).cuda() for x in (a, b, z0))
     out, lo, cnt = sgi.intersect_arc_lat_dw(da, db, dz, mode=mode)
