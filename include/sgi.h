@@ -123,7 +123,8 @@ size_t sgi_zonal_workspace_bytes(int64_t n_edges);
  * pair, Alg.1) and |n_xy|^2 as a pair (Alg.7):  lo = -((fma(hi, S2, X) + ((p - X) +
  * sigma)) + hi s2) / S2.  z needs no low part (P_z = z0 exactly).  Unused slots: canonical NaN.
  * mode must be SGI_MODE_EFT or SGI_MODE_EFT_LITERAL (else SGI_E_INVALID); other errors as for
- * sgi_intersect_arc_lat.  Device pointers, one launch on `stream`; not tuned. */
+ * sgi_intersect_arc_lat.  Device pointers, one launch on `stream` (TMA-staged when the batch is
+ * large and 16-B aligned, as for sgi_intersect_arc_lat). */
 sgi_status sgi_intersect_arc_lat_dw(const double* a, const double* b, const double* z0, int64_t n,
                                     int64_t ld, double* out_xyz, double* out_lo,
                                     uint8_t* out_count, int mode, void* stream);
