@@ -230,6 +230,26 @@ def test_edge_inputs(mode, omode):
     assert gcnt[14] == 0 and gcnt[15] == 0                     # NaN inputs: no points
 
 
+@pytest.mark.parametrize("mode,omode", MODES)
+@pytest.mark.parametrize("stride", [997, 2])
+def test_special_rows_on_the_tma_path(mode, omode, stride):
+    """The special rows (meridian arcs whose zero numerators fail the division guard, poles,
+    degenerate and NaN inputs, extreme scales) spread through a batch large enough for the
+    TMA-staged kernel, at odd and even positions: in the EFT modes each half of a thread's query
+    pair takes the Exact recompute on its own (stride 997), or both do (stride 2)."""
+    n = (1 << 19) + 321
+    a, b, z0 = sgi_inputs.generate_host(1, n)
+    sa, sb, sz = degenerate_and_special()
+    k = sz.shape[0]
+    idx = np.arange(5, n, stride)
+    a[:, idx] = sa[:, idx % k]
+    b[:, idx] = sb[:, idx % k]
+    z0[idx] = sz[idx % k]
+    got, gcnt = run_gpu(a, b, z0, mode)
+    ref, rcnt = oracle.intersect(omode, a, b, z0, nthreads=NTHREADS)
+    assert_parity(got, gcnt, ref, rcnt)
+
+
 def test_output_layout_and_canonical_nan():
     a, b, z0 = sgi_inputs.generate_host(5, 4096)
     got, gcnt = run_gpu(a, b, z0, "eft")
