@@ -383,6 +383,27 @@ def test_double_word_parity(config, n, mode, omode):
     assert np.array_equal(pcnt.cpu().numpy(), rcnt)
 
 
+@pytest.mark.parametrize("mode,omode", [("eft", oracle.MODE_EFT),
+                                        ("eft_literal", oracle.MODE_EFT_LITERAL)])
+@pytest.mark.parametrize("n", [20_000, (1 << 19) + 77])
+def test_double_word_special_rows(mode, omode, n):
+    """Double-word outputs with the special rows spread through the batch: the grid-stride
+    kernel (small n) and the TMA-staged one, both through their Exact recomputes."""
+    a, b, z0 = sgi_inputs.generate_host(1, n)
+    sa, sb, sz = degenerate_and_special()
+    idx = np.arange(3, n, 101)
+    a[:, idx] = sa[:, idx % sz.shape[0]]
+    b[:, idx] = sb[:, idx % sz.shape[0]]
+    z0[idx] = sz[idx % sz.shape[0]]
+    da, db, dz = (torch.from_numpy(x).cuda() for x in (a, b, z0))
+    out, lo, cnt = sgi.intersect_arc_lat_dw(da, db, dz, mode=mode)
+    torch.cuda.synchronize()
+    ref, rlo, rcnt = oracle.intersect_dw(omode, a, b, z0, nthreads=NTHREADS)
+    assert np.array_equal(cnt.cpu().numpy(), rcnt)
+    assert same(out.cpu().numpy(), ref).all()
+    assert same(lo.cpu().numpy(), rlo).all()
+
+
 def test_double_word_rejects_plain_modes():
     z = torch.zeros(8, dtype=torch.float64, device="cuda")
     v = torch.zeros((3, 8), dtype=torch.float64, device="cuda")
