@@ -285,6 +285,20 @@ def test_host_entry_matches_device_entry(mode):
     assert np.array_equal(c2, dcnt) and same(o2, dev).all()
 
 
+def test_host_entry_with_tma_sized_chunks():
+    """The e2e configuration: chunks of >= 2^19 queries (so every chunk runs the TMA-staged
+    kernel on the workspace's padded planes) and a ragged last chunk; equal to the device call."""
+    n = (1 << 23) + 5
+    a, b, z0 = sgi_inputs.generate_host(5, n)
+    dev, dcnt = run_gpu(a, b, z0, "eft")
+    pa, pb, pz = (torch.from_numpy(x).pin_memory() for x in (a, b, z0))
+    out = torch.empty((2, 3, n), dtype=torch.float64).pin_memory()
+    cnt = torch.empty(n, dtype=torch.uint8).pin_memory()
+    work = torch.empty(sgi.host_workspace_bytes(1 << 21), dtype=torch.uint8, device="cuda")
+    sgi.intersect_arc_lat_host(pa, pb, pz, mode="eft", out_xyz=out, out_count=cnt, work=work)
+    assert np.array_equal(cnt.numpy(), dcnt) and same(out.numpy(), dev).all()
+
+
 def test_side_stream_and_repeatability():
     n = 1 << 20
     da, db, dz = _device_config(5, n)
