@@ -32,8 +32,10 @@ BYTES_PER_ARC = 56 + 48 + 1          # a, b, z0 in; two xyz slots + uint8 count 
 # Algorithmic FP64 operations per query (add/sub/mul/fma/div/sqrt = 1 each) of the op sequence
 # in csrc/sgi_query.cuh; derivation in DESIGN.md §5.
 FP64_OPS = {"eft": 362, "eft_literal": 347, "naive": 42, "yac": 48, "base": 47, "naive_kahan": 45}
-SEEDS = {2: 2, 3: 3, 5: 5, 6: 6, 7: 7}
+SEEDS = {2: 2, 3: 3, 4: None, 5: 5, 6: 6, 7: 7}
+C4_PAIRS = 6_000_016   # C4: cubed sphere ne=1024 edges x 1,800 latitudes, materialised
 CONFIG_DESC = {
+    4: "C4 zonal-mean pairs (cubed sphere ne=1024 x 1,800 latitudes, materialised as arcs)",
     2: "C2 short arcs (midpoint uniform, length log-uniform [1e-4,1e-2] rad, z0 between endpoint z)",
     3: "C3 ill-conditioned arcs (near-tangent / near-polar / near-coincident thirds)",
     5: "C5 mixed arcs (50% C1, 25% C2, 25% uniform endpoints with z0 uniform in [-1,1])",
@@ -49,7 +51,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--mode", default="eft",
                    choices=["eft", "eft_literal", "naive", "yac", "base", "naive_kahan"])
-    p.add_argument("--config", type=int, default=2, choices=[2, 3, 5, 6, 7])
+    p.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5, 6, 7])
     p.add_argument("--n", type=int, default=1 << 24,
                    help="arcs per rank (--scaling weak) or in total (--scaling strong)")
     p.add_argument("--scaling", default="weak", choices=["weak", "strong"],
@@ -158,13 +160,43 @@ def pcie_concurrent_gbs(dev, nbytes=1 << 29):
     return best
 
 
+_C4 = {}
+
+
+def host_arcs(config: int, n: int, offset: int = 0):
+    """Arcs [offset, offset + n) of `config` on the host (C4: the materialised pair list)."""
+    import numpy as np
+    import sgi_inputs
+    if config == 4:
+        if not _C4:
+            a, b, z0, _ = sgi_inputs.c4_pairs(1024, 1800)
+            _C4.update(a=a, b=b, z0=z0)
+        sl = slice(offset, offset + n)
+        return (np.ascontiguousarray(_C4["a"][:, sl]), np.ascontiguousarray(_C4["b"][:, sl]),
+                np.ascontiguousarray(_C4["z0"][sl]))
+    return sgi_inputs.generate_host(config, n, offset=offset, seed=SEEDS[config])
+
+
+def device_arcs(config: int, n: int, a, b, z0, offset: int = 0):
+    """Fill device tensors with arcs [offset, offset + n) (C4 is built on the host and copied)."""
+    import torch
+    import sgi_inputs
+    if config == 4:
+        ha, hb, hz = host_arcs(4, n, offset)
+        a.copy_(torch.from_numpy(ha))
+        b.copy_(torch.from_numpy(hb))
+        z0.copy_(torch.from_numpy(hz))
+        return
+    sgi_inputs.generate_device(config, n, a, b, z0, offset=offset, seed=SEEDS[config])
+
+
 def cpu_baseline_run(config: int, n: int, mode: str):
     """Oracle (a) as it stands (oracle/eft_oracle.c, OpenMP over all host cores) on the whole
     per-rank batch of the same workload; returns (arcs/s, cores, seconds)."""
     import oracle
     import sgi_inputs
     cores = os.cpu_count() or 1
-    a, b, z0 = sgi_inputs.generate_host(config, n, seed=SEEDS[config])
+    a, b, z0 = host_arcs(config, n)
     m = {"eft": oracle.MODE_EFT, "eft_literal": oracle.MODE_EFT_LITERAL, "naive": oracle.MODE_NAIVE,
          "yac": oracle.MODE_YAC, "base": oracle.MODE_BASE, "naive_kahan": oracle.MODE_NAIVE_KAHAN}[mode]
     oracle.intersect(m, a[:, :4096], b[:, :4096], z0[:4096], nthreads=cores)   # warm
@@ -233,7 +265,7 @@ def run_reference(args):
     import sgi_inputs
     cores = os.cpu_count() or 1
     n = min(args.n, 1 << 22)
-    a, b, z0 = sgi_inputs.generate_host(args.config, n, seed=SEEDS[args.config])
+    a, b, z0 = host_arcs(args.config, n)
     m = {"eft": oracle.MODE_EFT, "eft_literal": oracle.MODE_EFT_LITERAL, "naive": oracle.MODE_NAIVE,
          "yac": oracle.MODE_YAC, "base": oracle.MODE_BASE,
          "naive_kahan": oracle.MODE_NAIVE_KAHAN}[args.mode]
@@ -335,7 +367,7 @@ def run_extra(args):
     a = torch.empty((3, n), dtype=torch.float64, device=dev)
     b = torch.empty_like(a)
     z0 = torch.empty(n, dtype=torch.float64, device=dev)
-    sgi_inputs.generate_device(cfg, n, a, b, z0, seed=SEEDS[cfg])
+    device_arcs(cfg, n, a, b, z0)
     cnt = torch.empty(n, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     L = sgi._load()
@@ -412,6 +444,9 @@ def main():
     if distributed:
         dist.init_process_group("nccl", device_id=dev)
     n, cfg, mode = args.n, args.config, args.mode
+    if cfg == 4:                                        # C4 is a fixed set: ranks split it
+        args.scaling, args.n = "strong", C4_PAIRS
+        n = C4_PAIRS
     if args.scaling == "weak":                          # this rank's slice of the index space
         offset, n = sdist.shard_weak(rank, ws, n)
     else:
@@ -422,7 +457,7 @@ def main():
     a = torch.empty((3, n), dtype=torch.float64, device=dev)
     b = torch.empty_like(a)
     z0 = torch.empty(n, dtype=torch.float64, device=dev)
-    sgi_inputs.generate_device(cfg, n, a, b, z0, offset=offset, seed=SEEDS[cfg])
+    device_arcs(cfg, n, a, b, z0, offset=offset)
     out = torch.empty((2, 3, n), dtype=torch.float64, device=dev)
     cnt = torch.empty(n, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
