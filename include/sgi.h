@@ -177,6 +177,17 @@ const char* sgi_status_str(sgi_status s);
 const char* sgi_last_error(void);
 int sgi_abi_version(void);
 
+/* Which kernel a call with these arguments launches (introspection for tests and profiling;
+ * no launch, no device access).  entry 0 = sgi_intersect_arc_lat, 1 = sgi_intersect_arc_lat_dw.
+ * SGI_PATH_LDG: the grid-stride kernel (batches below 2^19 queries, an odd ld, or inputs not
+ * 16-B aligned); SGI_PATH_TMA: the TMA-staged kernel, one query per thread; SGI_PATH_TMA_PAIR:
+ * the TMA-staged kernel with two adjacent queries per thread (EFT modes, entry 0, outputs
+ * 16-B aligned and out_count 2-B aligned).  SGI_PATH_NONE for n == 0 or arguments the entry
+ * would reject.  Every path gives the same outputs bit for bit (up to the sign of zero). */
+enum { SGI_PATH_NONE = 0, SGI_PATH_LDG = 1, SGI_PATH_TMA = 2, SGI_PATH_TMA_PAIR = 3 };
+int sgi_dispatch_path(const double* a, const double* b, const double* z0, int64_t n, int64_t ld,
+                      const double* out_xyz, const uint8_t* out_count, int mode, int entry);
+
 #ifdef __cplusplus
 }
 #endif

@@ -30,6 +30,8 @@ TRACE_FIELDS = ("nx", "ex", "ny", "ey", "nz", "ez", "S2", "s2", "S3", "s3", "C",
                 "Xp_p", "Xp_s", "Yp_p", "Yp_s", "Xm_p", "Xm_s", "Ym_p", "Ym_s")
 DEGENERATE = 0xFF
 SGI_OK, SGI_E_INVALID, SGI_E_CUDA = 0, 1, 2
+# sgi_dispatch_path results (include/sgi.h SGI_PATH_*)
+PATHS = {0: "none", 1: "ldg", 2: "tma", 3: "tma_pair"}
 
 _lib = None
 
@@ -74,6 +76,8 @@ def _load():
         L.sgi_last_error.argtypes = []
         L.sgi_abi_version.restype = ctypes.c_int
         L.sgi_abi_version.argtypes = []
+        L.sgi_dispatch_path.restype = ctypes.c_int
+        L.sgi_dispatch_path.argtypes = [vp, vp, vp, i64, i64, vp, vp, ctypes.c_int, ctypes.c_int]
         _lib = L
     return _lib
 
@@ -118,6 +122,14 @@ def _cuda_f64(t, shape, name):
         raise ValueError(f"{name} must be a contiguous CUDA float64 tensor of shape {shape}")
 
 
+def _cuda_u8(t, name, shape=None):
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.uint8
+            and t.is_contiguous() and t.dim() == 1 and (shape is None or tuple(t.shape) == shape)):
+        raise ValueError(f"{name} must be a contiguous 1-D CUDA uint8 tensor"
+                         + (f" of shape {shape}" if shape else ""))
+
+
 def intersect_arc_lat(a, b, z0, mode="eft", out_xyz=None, out_count=None, n=None, stream=None):
     """Device entry: torch CUDA tensors a[3, ld], b[3, ld], z0[ld] -> (out_xyz[2,3,ld], out_count[ld]).
 
@@ -133,8 +145,7 @@ def intersect_arc_lat(a, b, z0, mode="eft", out_xyz=None, out_count=None, n=None
     if out_count is None:
         out_count = torch.empty(ld, dtype=torch.uint8, device=z0.device)
     _cuda_f64(out_xyz, (2, 3, ld), "out_xyz")
-    if not (out_count.is_cuda and out_count.dtype == torch.uint8 and out_count.shape == (ld,)):
-        raise ValueError("out_count must be a CUDA uint8 tensor of shape (ld,)")
+    _cuda_u8(out_count, "out_count", (ld,))
     rc = _load().sgi_intersect_arc_lat(a.data_ptr(), b.data_ptr(), z0.data_ptr(), n, ld,
                                        out_xyz.data_ptr(), out_count.data_ptr(), _mode(mode),
                                        _stream_ptr(stream))
@@ -168,6 +179,14 @@ def output_stats(out_xyz, out_count, z0, ref_xyz=None, ref_count=None, n=None, s
     import torch
     ld = z0.shape[0]
     n = ld if n is None else n
+    _cuda_f64(z0, (ld,), "z0")
+    _cuda_f64(out_xyz, (2, 3, ld), "out_xyz")
+    _cuda_u8(out_count, "out_count", (ld,))
+    if (ref_xyz is None) != (ref_count is None):
+        raise ValueError("give both ref_xyz and ref_count, or neither")
+    if ref_xyz is not None:
+        _cuda_f64(ref_xyz, (2, 3, ld), "ref_xyz")
+        _cuda_u8(ref_count, "ref_count", (ld,))
     dev = z0.device
     if stats is None:
         stats = torch.zeros(2, dtype=torch.float64, device=dev)
@@ -200,6 +219,32 @@ def intersect_trace(a, b, z0, mode="eft", n=None, stream=None):
     return trace, cnt
 
 
+def dispatch_path(a, b, z0, out_xyz, out_count, mode="eft", n=None, entry=0) -> str:
+    """Which kernel sgi_intersect_arc_lat (entry 0) or sgi_intersect_arc_lat_dw (entry 1) launches
+    for these tensors: "ldg", "tma" (one query per thread) or "tma_pair" (two per thread)."""
+    ld = z0.shape[0]
+    n = ld if n is None else n
+    return PATHS[_load().sgi_dispatch_path(a.data_ptr(), b.data_ptr(), z0.data_ptr(), n, ld,
+                                           out_xyz.data_ptr(), out_count.data_ptr(), _mode(mode),
+                                           entry)]
+
+
+def _host_array(x, shape, dtype, name):
+    """Host buffer check for the host-buffer entry: C-contiguous numpy array or CPU tensor of
+    exactly this shape and dtype (the C side reads/writes ld-pitched planes through it)."""
+    import numpy as np
+    import torch
+    if isinstance(x, torch.Tensor):
+        tdt = {np.float64: torch.float64, np.uint8: torch.uint8}[dtype]
+        ok = (x.device.type == "cpu" and x.dtype == tdt and x.is_contiguous()
+              and tuple(x.shape) == shape)
+        return ok and x.data_ptr()
+    if isinstance(x, np.ndarray):
+        ok = x.dtype == dtype and x.flags.c_contiguous and x.shape == shape
+        return ok and x.ctypes.data
+    return False
+
+
 def host_workspace_bytes(chunk: int) -> int:
     return int(_load().sgi_host_workspace_bytes(chunk))
 
@@ -213,21 +258,32 @@ def intersect_arc_lat_host(a, b, z0, mode="eft", out_xyz=None, out_count=None, w
     import numpy as np
     import torch
 
-    def ptr(x):
-        return x.data_ptr() if isinstance(x, torch.Tensor) else x.ctypes.data
-
     ld = z0.shape[0]
     n = ld if n is None else n
+    if not 0 <= n <= ld:
+        raise ValueError(f"need 0 <= n <= ld, got n={n}, ld={ld}")
     if out_xyz is None:
         out_xyz = np.empty((2, 3, ld), np.float64)
     if out_count is None:
         out_count = np.empty(ld, np.uint8)
+    ptrs = []
+    for x, shape, dt, name in ((a, (3, ld), np.float64, "a"), (b, (3, ld), np.float64, "b"),
+                               (z0, (ld,), np.float64, "z0"),
+                               (out_xyz, (2, 3, ld), np.float64, "out_xyz"),
+                               (out_count, (ld,), np.uint8, "out_count")):
+        p = _host_array(x, shape, dt, name)
+        if p is False:
+            raise ValueError(f"{name} must be a C-contiguous host {np.dtype(dt).name} array "
+                             f"(numpy or CPU tensor) of shape {shape}")
+        ptrs.append(p)
     if work is None:
         work = torch.empty(host_workspace_bytes(min(max(n, 1), 1 << 22)), dtype=torch.uint8,
                            device="cuda")
-    rc = _load().sgi_intersect_arc_lat_host(ptr(a), ptr(b), ptr(z0), n, ld, ptr(out_xyz),
-                                            ptr(out_count), _mode(mode), work.data_ptr(),
-                                            work.numel(), _stream_ptr(stream))
+    if not (isinstance(work, torch.Tensor) and work.is_cuda and work.is_contiguous()):
+        raise ValueError("work must be a contiguous CUDA tensor")
+    rc = _load().sgi_intersect_arc_lat_host(*ptrs[:3], n, ld, *ptrs[3:], _mode(mode),
+                                            work.data_ptr(), work.numel() * work.element_size(),
+                                            _stream_ptr(stream))
     _check(rc, "sgi_intersect_arc_lat_host")
     return out_xyz, out_count
 
@@ -235,9 +291,15 @@ def intersect_arc_lat_host(a, b, z0, mode="eft", out_xyz=None, out_count=None, w
 def count_histogram(out_count, n=None, hist=None, stream=None):
     """Device histogram [#0, #1, #2, #degenerate, #points] (int64 CUDA tensor, accumulated)."""
     import torch
+    _cuda_u8(out_count, "out_count")
     n = out_count.shape[0] if n is None else n
+    if not 0 <= n <= out_count.shape[0]:
+        raise ValueError(f"n={n} outside out_count's length {out_count.shape[0]}")
     if hist is None:
         hist = torch.zeros(5, dtype=torch.int64, device=out_count.device)
+    if not (hist.is_cuda and hist.dtype == torch.int64 and hist.is_contiguous()
+            and tuple(hist.shape) == (5,)):
+        raise ValueError("hist must be a contiguous CUDA int64 tensor of shape (5,)")
     rc = _load().sgi_count_histogram(out_count.data_ptr(), n, hist.data_ptr(), _stream_ptr(stream))
     _check(rc, "sgi_count_histogram")
     return hist

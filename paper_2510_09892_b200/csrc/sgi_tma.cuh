@@ -28,6 +28,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Stage release counter: an acquire-release add on a shared counter (PTX memory model).  Each
+// warp's lane 0 adds after __syncwarp() (which orders the warp's shared-memory reads of the
+// stage before it); the release publishes those reads, and the last warp's acquire makes them
+// happen-before its fence.proxy.async and the bulk copy that overwrites the stage (no WAR race
+// between the generic-proxy reads and the async-proxy write).
+__device__ __forceinline__ uint32_t stage_arrive(int* counter) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old)
+               : "r"(smem_u32(counter)) : "memory");
+  return old;
+}
+
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");

@@ -443,7 +443,9 @@ __device__ __forceinline__ void run_batch(const WarpQueue& q, int n, const doubl
   };
   if constexpr (kHalves == 2 && (MODE == sgi::MODE_EFT || MODE == sgi::MODE_EFT_LITERAL)) {
     const sgi::SmemIn2 in = {smem_u32(&q.v[0][lane][0]), (uint32_t)sizeof(q.v[0])};
-    const sgi::W2 zz = {tab[q.lat[lane]], tab[q.lat[lane + 32]]};
+    // items >= n hold stale or never-written latitude indices: read the table only for live
+    // items (entry 0 otherwise; their results are never stored)
+    const sgi::W2 zz = {tab[lane < n ? q.lat[lane] : 0], tab[lane + 32 < n ? q.lat[lane + 32] : 0]};
     sgi::QueryOut2 o;
     const sgi::B2 ok = sgi::query_fast2<MODE>(in, zz, o);
     store({o.p0x.x, o.p0y.x, o.p1x.x, o.p1y.x, o.count[0]}, zz.x, ok.x, lane);
@@ -452,7 +454,7 @@ __device__ __forceinline__ void run_batch(const WarpQueue& q, int n, const doubl
 #pragma unroll
     for (int h = 0; h < kHalves; ++h) {
       const sgi::SmemIn in1 = {smem_u32(&q.v[0][lane][h]), (uint32_t)sizeof(q.v[0])};
-      const double z0 = tab[q.lat[lane + 32 * h]];
+      const double z0 = tab[lane + 32 * h < n ? q.lat[lane + 32 * h] : 0];
       sgi::QueryOut o;
       const bool ok = sgi::query_fast<MODE>(in1, z0, o);
       store(o, z0, ok, lane + 32 * h);

@@ -29,7 +29,7 @@ def test_header_declares_the_boundary():
         "sgi_intersect_arc_lat", "sgi_intersect_arc_lat_host", "sgi_host_workspace_bytes",
         "sgi_count_histogram", "sgi_status_str", "sgi_last_error", "sgi_abi_version",
         "sgi_zonal_intersect", "sgi_zonal_workspace_bytes", "sgi_intersect_trace",
-        "sgi_trace_fields", "sgi_output_stats", "sgi_intersect_arc_lat_dw"])
+        "sgi_trace_fields", "sgi_output_stats", "sgi_intersect_arc_lat_dw", "sgi_dispatch_path"])
 
 
 def test_library_exports_every_declared_symbol(lib):
@@ -101,6 +101,48 @@ def test_host_entry_validates_workspace(lib):
     P = lambda x: x.ctypes.data  # noqa: E731
     rc = lib.sgi_intersect_arc_lat_host(P(a), P(b), P(z), n, n, P(out), P(cnt), 1, None, 0, None)
     assert rc == sgi.SGI_E_INVALID
+
+
+def test_dispatch_path_rules(lib):
+    """The kernel choice (no device access): LDG below 2^19 queries, for an odd ld or inputs not
+    16-B aligned; the TMA pair kernel in the EFT modes with 16-B aligned outputs; the one-query
+    TMA kernel otherwise; the double-word entry never pairs."""
+    D = lib.sgi_dispatch_path
+    n = 1 << 20
+    base = 1 << 40                                   # fake, well separated 256-B aligned bases
+    a, b, z, out, cnt = (base + k * (1 << 34) for k in range(5))
+    eft, lit, naive = 1, 2, 0
+    assert D(a, b, z, n, n, out, cnt, eft, 0) == 3
+    assert D(a, b, z, n, n, out, cnt, lit, 0) == 3
+    assert D(a, b, z, n, n, out, cnt, naive, 0) == 2
+    assert D(a, b, z, n, n, out + 8, cnt, eft, 0) == 2        # 8-B aligned outputs: one query
+    assert D(a, b, z, n, n, out, cnt + 1, eft, 0) == 2        # odd count base: one query
+    assert D(a + 8, b, z, n, n, out, cnt, eft, 0) == 1        # 8-B aligned inputs: LDG
+    assert D(a, b, z, n - 1, n - 1, out, cnt, eft, 0) == 1    # odd ld: LDG
+    assert D(a, b, z, n - 1, n, out, cnt, eft, 0) == 3        # odd n, even ld: TMA + tail
+    assert D(a, b, z, (1 << 19) - 2, 1 << 19, out, cnt, eft, 0) == 1   # small batch
+    assert D(a, b, z, n, n, out, cnt, eft, 1) == 2            # double-word: one query / thread
+    assert D(a, b, z, n, n, out, cnt, naive, 1) == 0          # double-word needs an EFT mode
+    assert D(a, b, z, 0, 0, out, cnt, eft, 0) == 0
+    assert D(a, b, z, n, n, a, cnt, eft, 0) == 0              # aliasing: rejected
+    assert D(a, b, z, n, n - 2, out, cnt, eft, 0) == 0        # ld < n: rejected
+
+
+def test_host_binding_validates_host_arrays():
+    """The host-buffer binding checks dtype, shape and contiguity before any pointer reaches C
+    (a wrong array would make the 2D copies read or write past the host buffers)."""
+    n = 64
+    a = np.zeros((3, n)); b = np.zeros((3, n)); z = np.zeros(n)
+    bad = [dict(a=a.astype(np.float32)), dict(a=np.zeros((n, 3))), dict(b=np.zeros((3, 2 * n))[:, ::2]),
+           dict(out_xyz=np.zeros((2, 3, n), np.float32)), dict(out_count=np.zeros(n, np.int32)),
+           dict(z0=np.zeros(n + 1), a=np.zeros((3, n + 1)), b=np.zeros((3, n)))]
+    for kw in bad:
+        args = dict(a=a, b=b, z0=z)
+        args.update(kw)
+        with pytest.raises(ValueError):
+            sgi.intersect_arc_lat_host(args.pop("a"), args.pop("b"), args.pop("z0"), **args)
+    with pytest.raises(ValueError):
+        sgi.intersect_arc_lat_host(a, b, z, n=n + 1)
 
 
 def test_product_package_does_not_import_oracle():
