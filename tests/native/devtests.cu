@@ -149,8 +149,27 @@ __global__ void devprim_kernel(int op, int k, const double* in, int width, int64
         for (int j = 1; j < k; ++j) sgi::cdc_step(P.hi, P.lo, r[j], r[k + j]);
         p = op == 9 ? P : sgi::dd{sgi::add(P.hi, P.lo), 0.0};
       } break;
+      case 11: {   // certified numerators (policy Cert): row [F, eF, v, ev, z0, s, es]
+        double Xp, Xm;
+        bool ok = true;
+        sgi::numerators_cert(r[0], r[1], r[2], r[3], r[4], r[5], r[6], Xp, Xm, ok);
+        p = ok ? sgi::dd{Xp, Xm} : sgi::dd{sgi::qnan(), sgi::qnan()};
+      } break;
+      case 12: {   // the same through the two-lane type (rows i and i + n/2 as one W2 pair)
+        if (i >= n / 2) break;
+        const double* q = in + (i + n / 2) * width;
+        sgi::W2 Xp, Xm;
+        sgi::B2 ok = {true, true};
+        sgi::numerators_cert(sgi::W2{r[0], q[0]}, sgi::W2{r[1], q[1]}, sgi::W2{r[2], q[2]},
+                             sgi::W2{r[3], q[3]}, sgi::W2{r[4], q[4]}, sgi::W2{r[5], q[5]},
+                             sgi::W2{r[6], q[6]}, Xp, Xm, ok);
+        out[2 * (i + n / 2)] = ok.y ? Xp.y : sgi::qnan();
+        out[2 * (i + n / 2) + 1] = ok.y ? Xm.y : sgi::qnan();
+        p = ok.x ? sgi::dd{Xp.x, Xm.x} : sgi::dd{sgi::qnan(), sgi::qnan()};
+      } break;
       default: break;
     }
+    if (op == 12 && i >= n / 2) continue;
     out[2 * i] = p.hi;
     out[2 * i + 1] = p.lo;
   }

@@ -90,3 +90,68 @@ def test_device_primitives_equal_oracle(name):
         assert keep.mean() > 0.97
         same = (got[keep] == ref[keep]) | (np.isnan(got[keep]) & np.isnan(ref[keep]))
         assert same.all(), f"{name} fast={fast}: {int((~same).sum())} values differ"
+
+
+# ---------------------------------- certified numerators (policy Cert, DESIGN.md §5 L7)
+U = 2.0 ** -53
+
+
+def cert_rows(n, rng, near_ties):
+    """Rows [F, eF, v, ev, z0, s, es] with SGI_MODE_EFT's magnitude relations (|eF| <= 3u|F|,
+    |ev| <= u|v|, |es| <= 1.5u|s|) and spread exponents; with near_ties, es is re-chosen (exact
+    rationals) so that the + root's exact dot product V = (F + eF) z0 + (v + ev)(s + es) lies
+    within ~u^2 |v s| of a rounding boundary of X+ (a midpoint between adjacent doubles): the
+    regime where the guard must fail or be right."""
+    from fractions import Fraction as Fr
+    import math
+    F = rng.uniform(0.5, 1, n) * 2.0 ** rng.integers(-40, 10, n) * rng.choice([-1, 1], n)
+    z0 = rng.uniform(-1, 1, n)
+    v = rng.uniform(0.5, 1, n) * 2.0 ** rng.integers(-40, 10, n) * rng.choice([-1, 1], n)
+    s = np.abs(F * z0 / v) * rng.uniform(0.01, 4, n)      # v s comparable to F z0: cancellations
+    eF = F * rng.uniform(-3, 3, n) * U
+    ev = v * rng.uniform(-1, 1, n) * U
+    es = s * rng.uniform(-1, 1, n) * U
+    if near_ties:
+        for i in range(n):
+            K = (Fr(F[i]) + Fr(eF[i])) * Fr(z0[i]) + (Fr(v[i]) + Fr(ev[i])) * Fr(s[i])
+            cv = Fr(v[i]) + Fr(ev[i])
+            X0 = float(K + cv * Fr(es[i]))
+            if X0 == 0.0:
+                continue
+            m = Fr(X0) + Fr(math.ulp(X0)) / 2 * (1 if rng.random() < 0.5 else -1)
+            e2 = float((m - K) / cv)
+            if abs(e2) <= 1.5 * U * abs(s[i]):
+                es[i] = e2
+    return np.ascontiguousarray(np.stack([F, eF, v, ev, z0, s, es], axis=1))
+
+
+@pytest.mark.parametrize("op", [11, 12])
+@pytest.mark.parametrize("near_ties", [False, True])
+def test_certified_numerators_equal_compdot(op, near_ties):
+    """Policy Cert's numerators either equal the paper's CompDot (oracle (a), bit for bit) or
+    report failure (then the query is recomputed with the listing's sequence); near ties the
+    guard must fire, so the test also checks that it does.  op 12 runs the two-lane (W2) type."""
+    lib = ctypes.CDLL(build_devtests())
+    lib.sgi_devprim.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
+                                ctypes.c_int64, ctypes.c_void_p, ctypes.c_int]
+    rng = np.random.default_rng(11 + near_ties)
+    n = 20_000 if near_ties else 400_000
+    rows = cert_rows(n, rng, near_ties)
+    F, eF, v, ev, z0, s, es = rows.T
+    w = np.stack([z0, z0, s, s, es, es], axis=1)
+    ref = np.empty((n, 2))
+    for k, sg in enumerate((1.0, -1.0)):
+        x = np.stack([F, eF, sg * v, sg * ev, sg * v, sg * ev], axis=1)
+        ref[:, k] = oracle.prim("comp_dot", np.ascontiguousarray(np.hstack([x, w])), 6)[:, 0]
+    din = torch.from_numpy(rows).cuda()
+    dout = torch.empty((n, 2), dtype=torch.float64, device="cuda")
+    assert lib.sgi_devprim(op, 0, ctypes.c_void_p(din.data_ptr()), 7, n,
+                           ctypes.c_void_p(dout.data_ptr()), 0) == 0
+    got = dout.cpu().numpy()
+    ok = ~np.isnan(got[:, 0])
+    same = (got[ok] == ref[ok])
+    assert same.all(), f"{int((~same).sum())} certified numerators differ from CompDot"
+    if near_ties:
+        assert (~ok).mean() > 0.2, f"guard fired on only {(~ok).mean():.3f} of near-tie rows"
+    else:
+        assert ok.mean() > 0.999
