@@ -23,13 +23,15 @@ def run_bench(*args, timeout=600):
 
 
 def test_default_line_has_every_key():
-    d = run_bench("--steps", "20", "--warmup", "3", "--e2e-steps", "2")
+    """The default workload (C5, strong scaling) at a 2^24-arc batch to keep the test short."""
+    d = run_bench("--steps", "20", "--warmup", "3", "--e2e-steps", "2", "--n", str(1 << 24))
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
               "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "roofline",
               "cpu_baseline", "e2e", "clocks", "gpu_launches"):
         assert k in d, k
     assert d["n_gpus"] == 1 and d["steps"] == 20 and d["warmup"] >= 3
-    assert d["higher_is_better"] is True and d["scaling"] == "weak" and d["dtype"] == "f64"
+    assert d["higher_is_better"] is True and d["scaling"] == "strong" and d["dtype"] == "f64"
+    assert d["config"]["workload"].startswith("C5") and d["config"]["kernel"] == "tma_pair"
     assert d["value"] > 1e10 and d["ms_per_step"] > 0
     assert "workload" in d["config"] and "l2" in d["config"]
     r = d["roofline"]
@@ -43,6 +45,16 @@ def test_default_line_has_every_key():
     assert 0 < e["value"] < d["value"]
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert d["gpu_launches"] == 20
+    acc = d["max_ulp_err"]
+    assert acc["eft"]["max_err_u"] <= 3.0 and acc["eft"]["over_bound"] == 0
+    assert acc["eft"]["count_mismatch_vs_exact"] == 0
+    assert d["hist"]["zero"] > 0 and d["hist"]["two"] > 0       # C5 mixes 0/1/2 points
+
+
+def test_weak_c2_line():
+    d = run_bench("--config", "2", "--steps", "10", "--warmup", "3", "--e2e-steps", "0",
+                  "--no-cpu-baseline")
+    assert d["scaling"] == "weak" and d["config"]["arcs_per_rank"] == 1 << 24
     assert d["max_ulp_err"]["eft"]["max_err_u"] <= 3.0
 
 

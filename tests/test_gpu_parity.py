@@ -356,6 +356,55 @@ def test_sharding_is_rank_invariant():
         assert torch.equal(hist, hist_ref)
 
 
+def test_bench_strong_split_dry_run():
+    """bench.py's own strong-scaling path on one device, R = 1, 2, 4, 8 ranks run one after the
+    other: dist.shard_strong slices, device generation at the slice offset (bench.device_arcs),
+    the EFT kernel, the histogram, the chunked K5 statistics against naive
+    (bench.ref_mode_chunks) and the accuracy sample indices (dist.sample_indices); the per-rank
+    results combined as reduce_after_step / reduce_accuracy combine them (SUM of histograms
+    and counts, MAX of statistics) equal the R = 1 results.  This is the 1/2/4/8-GPU run's
+    data path without the NCCL transport."""
+    import bench
+    from paper_2510_09892_b200 import dist as sdist
+    n = (1 << 22) + 6                       # C5 layout, a ragged split
+    L = sgi._load()
+    stream = torch.cuda.current_stream()
+    results = {}
+    for R in (1, 2, 4, 8):
+        hist = torch.zeros(5, dtype=torch.int64, device="cuda")
+        stats = torch.zeros(2, dtype=torch.float64, device="cuda")
+        counts = torch.zeros(2, dtype=torch.int64, device="cuda")
+        sample = []
+        for r in range(R):
+            off, m = sdist.shard_strong(r, R, n)
+            a = torch.empty((3, m), dtype=torch.float64, device="cuda")
+            b = torch.empty_like(a)
+            z0 = torch.empty(m, dtype=torch.float64, device="cuda")
+            bench.device_arcs(5, m, a, b, z0, offset=off)
+            out = torch.empty((2, 3, m), dtype=torch.float64, device="cuda")
+            cnt = torch.empty(m, dtype=torch.uint8, device="cuda")
+            sgi.intersect_arc_lat(a, b, z0, mode="eft", out_xyz=out, out_count=cnt)
+            h = sgi.count_histogram(cnt)
+            st, ct = bench.ref_mode_chunks(L, a, b, z0, m, out, cnt, "eft", "naive", stream, sgi,
+                                           chunk=1 << 20)
+            hist += h
+            stats = torch.maximum(stats, st)
+            counts += ct
+            idx = sdist.sample_indices(n, 2000, off, m)
+            ti = torch.from_numpy(idx).cuda()
+            sample.append((out.index_select(-1, ti).cpu(), cnt.index_select(0, ti).cpu()))
+        t = torch.zeros(1, dtype=torch.float64, device="cuda")
+        sdist.reduce_after_step(t, hist, stats, counts)     # no process group: identity
+        results[R] = (hist.cpu(), stats.cpu(), counts.cpu(),
+                      torch.cat([o for o, _ in sample], -1), torch.cat([c for _, c in sample]))
+    h1, s1, c1, o1, k1 = results[1]
+    assert h1[:4].sum() == n and h1[0] > 0 and h1[1] > 0 and h1[2] > 0
+    for R in (2, 4, 8):
+        h, st, ct, o, k = results[R]
+        assert torch.equal(h, h1) and torch.equal(ct, c1) and torch.equal(st, s1), R
+        assert torch.equal(k, k1) and torch.equal(o.view(torch.int64), o1.view(torch.int64)), R
+
+
 def test_histogram_matches_bincount():
     a, b, z0 = sgi_inputs.generate_host(5, 200_000)
     da, db, dz = (torch.from_numpy(x).cuda() for x in (a, b, z0))
