@@ -167,6 +167,14 @@ __global__ void devprim_kernel(int op, int k, const double* in, int width, int64
         out[2 * (i + n / 2) + 1] = ok.y ? Xm.y : sgi::qnan();
         p = ok.x ? sgi::dd{Xp.x, Xm.x} : sgi::dd{sgi::qnan(), sgi::qnan()};
       } break;
+      case 13: {   // policy Cert's front: row [nx, ex, ny, ey, nz, ez, z0] -> (S2, sigma_h)
+        sgi::EdgePreT<double> e;
+        e.nx = {r[0], r[1]}; e.ny = {r[2], r[3]}; e.nz = {r[4], r[5]};
+        sgi::cert_sums(e);
+        bool ok = true;
+        const sgi::CertFront<double> f = sgi::cert_sigma(e, r[6], ok);
+        p = ok ? sgi::dd{f.S2, f.sh} : sgi::dd{sgi::qnan(), sgi::qnan()};
+      } break;
       default: break;
     }
     if (op == 12 && i >= n / 2) continue;

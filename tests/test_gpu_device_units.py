@@ -155,3 +155,86 @@ def test_certified_numerators_equal_compdot(op, near_ties):
         assert (~ok).mean() > 0.2, f"guard fired on only {(~ok).mean():.3f} of near-tie rows"
     else:
         assert ok.mean() > 0.999
+
+
+def cert_front_rows(n, rng, target):
+    """Rows [nx, ex, ny, ey, nz, ez, z0] shaped like SGI_MODE_EFT's renormalised normal pairs
+    (|e| <= u|n|) with z0 inside the circle's z-range.  target "S2" / "sigma": ey / ez re-chosen
+    (exact rationals) so that nx^2 + ny^2 + 2(nx ex + ny ey) -- resp. that minus
+    (|n|^2 + 2 n.e) z0^2 -- lies within ~u^2 of a rounding boundary of the listing's rounded
+    |n_xy|^2 -- resp. s^2 -- where the certificate must fail or be right."""
+    from fractions import Fraction as Fr
+    import math
+    n3 = rng.normal(size=(n, 3)) * 2.0 ** rng.integers(-30, 1, (n, 1))
+    n3[:, 2] *= rng.uniform(0.5, 2.0, n)
+    e3 = n3 * rng.uniform(-1, 1, (n, 3)) * U
+    S = n3[:, 0] ** 2 + n3[:, 1] ** 2
+    N = S + n3[:, 2] ** 2
+    z0 = rng.uniform(-1, 1, n) * np.sqrt(S / N)
+    if target is not None:
+        for i in range(n):
+            nx, ny, nz = (Fr(v) for v in n3[i])
+            ex, ey, ez = (Fr(v) for v in e3[i])
+            z2 = Fr(z0[i]) ** 2
+            S2 = nx * nx + ny * ny + 2 * (nx * ex + ny * ey)
+            sgn = 1 if rng.random() < 0.5 else -1
+            if target == "S2":
+                h = float(S2)
+                m = Fr(h) + sgn * Fr(math.ulp(h)) / 2
+                new = float((m - nx * nx - ny * ny - 2 * nx * ex) / (2 * ny))
+                if abs(new) <= U * abs(n3[i, 1]):
+                    e3[i, 1] = new
+            else:
+                sig = S2 - (S2 + nz * nz + 2 * nz * ez) * z2
+                h = float(sig)
+                if h <= 0 or z2 == 0 or nz == 0:
+                    continue
+                m = Fr(h) + sgn * Fr(math.ulp(h)) / 2
+                rest = S2 - (S2 + nz * nz) * z2
+                new = float((rest - m) / (2 * nz * z2))
+                if abs(new) <= U * abs(n3[i, 2]):
+                    e3[i, 2] = new
+    return np.ascontiguousarray(np.stack([n3[:, 0], e3[:, 0], n3[:, 1], e3[:, 1], n3[:, 2],
+                                          e3[:, 2], z0], axis=1))
+
+
+def listing_front(rows):
+    """The listing's S2 and s^2 high part (AccuX lines 5-11) from oracle (a)'s operators."""
+    nx, ex, ny, ey, nz, ez, z0 = rows.T
+    S2 = oracle.prim("sum_of_squares_c", np.ascontiguousarray(np.stack([nx, ny, ex, ey], 1)), 2)
+    S3 = oracle.prim("sum_of_squares_c",
+                     np.ascontiguousarray(np.stack([nx, ny, nz, ex, ey, ez], 1)), 3)
+    C = oracle.prim("two_prod", np.ascontiguousarray(np.stack([z0, z0], 1)))
+    D = oracle.prim("comp_dot_c", np.ascontiguousarray(np.stack(
+        [S3[:, 0], S3[:, 0], S3[:, 1], S3[:, 1], C[:, 0], C[:, 1], C[:, 0], C[:, 1]], 1)), 4)
+    E = oracle.prim("two_sum", np.ascontiguousarray(np.stack([S2[:, 0], -D[:, 0]], 1)))
+    e = (S2[:, 1] - D[:, 1]) + E[:, 1]
+    sig = oracle.prim("fast_two_sum", np.ascontiguousarray(np.stack([E[:, 0], e], 1)))
+    return S2[:, 0], sig[:, 0]
+
+
+@pytest.mark.parametrize("target", [None, "S2", "sigma"])
+def test_certified_front_equals_listing(target):
+    """Policy Cert's |n_xy|^2 high part and s^2 high part either equal the listing's
+    (SumOfSquaresC, CompDotC, TwoSum chain of AccuX lines 5-11 by oracle (a)'s operators) bit
+    for bit or report failure; rows placed at rounding boundaries must make the certificate
+    fire."""
+    lib = ctypes.CDLL(build_devtests())
+    lib.sgi_devprim.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
+                                ctypes.c_int64, ctypes.c_void_p, ctypes.c_int]
+    rng = np.random.default_rng({None: 21, "S2": 22, "sigma": 23}[target])
+    n = 400_000 if target is None else 20_000
+    rows = cert_front_rows(n, rng, target)
+    S2, sh = listing_front(rows)
+    din = torch.from_numpy(rows).cuda()
+    dout = torch.empty((n, 2), dtype=torch.float64, device="cuda")
+    assert lib.sgi_devprim(13, 0, ctypes.c_void_p(din.data_ptr()), 7, n,
+                           ctypes.c_void_p(dout.data_ptr()), 0) == 0
+    got = dout.cpu().numpy()
+    ok = ~np.isnan(got[:, 0])
+    assert (got[ok, 0] == S2[ok]).all(), int((got[ok, 0] != S2[ok]).sum())
+    assert (got[ok, 1] == sh[ok]).all(), int((got[ok, 1] != sh[ok]).sum())
+    if target is None:
+        assert ok.mean() > 0.999
+    else:
+        assert (~ok).mean() > 0.2, f"certificate fired on only {(~ok).mean():.3f} of the rows"
