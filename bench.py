@@ -29,9 +29,11 @@ sys.path.insert(0, ROOT)
 METRIC = "EFT arc-latitude intersections/s (FP64) at 1/2/4/8 B200; % roofline; max ulp err"
 UNIT = "intersections/s"
 BYTES_PER_ARC = 56 + 48 + 1          # a, b, z0 in; two xyz slots + uint8 count out (§8(b))
-# Algorithmic FP64 operations per query (add/sub/mul/fma/div/sqrt = 1 each) of the op sequence
-# in csrc/sgi_query.cuh; derivation in DESIGN.md §5.
-FP64_OPS = {"eft": 362, "eft_literal": 347, "naive": 42, "yac": 48, "base": 47, "naive_kahan": 45}
+# Algorithmic FP64 operations per query (add/sub/mul/fma/div/sqrt/compare = 1 each) of the
+# paper's listing: AccuX both roots 334 + renormalisation 18 + containment 14 = 366
+# (DESIGN.md §5 reading of the count); literal 351, naive 46.  The plain-binary64 variants count
+# their own listings.
+FP64_OPS = {"eft": 366, "eft_literal": 351, "naive": 46, "yac": 52, "base": 51, "naive_kahan": 49}
 SEEDS = {2: 2, 3: 3, 4: None, 5: 5, 6: 6, 7: 7}
 C4_PAIRS = 6_000_016   # C4: cubed sphere ne=1024 edges x 1,800 latitudes, materialised
 CONFIG_DESC = {
@@ -595,28 +597,45 @@ def main():
                     ref_mode: {"max_err_u": w[1], "over_bound": sm[3],
                                "count_mismatch_vs_exact": sm[4]}}
 
-    # roofline of the dominant (only) kernel, bound = the slower of the two roofs
+    # roofline of the dominant (only) kernel: bound = the slower of the HBM roof (105 B/query)
+    # and the FP64 roof at the FP64-pipe instructions the shipped kernel executes per query
+    # (ncu, profiles/fp64_sass.json; the listing's algorithmic count where none is measured)
     peaks = load_peaks()
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     alu_peak = sms * 64 * peaks["sm_max_mhz"] * 1e6 / 1e12     # T FP64 instr/s (64 lanes/SM)
-    hbm_bytes, ops = n * BYTES_PER_ARC, n * FP64_OPS[mode]
+    sass = {}
+    spath = os.path.join(ROOT, "profiles", "fp64_sass.json")
+    if os.path.exists(spath):
+        with open(spath) as f:
+            sass = json.load(f)
+    per_q = sass.get(mode, FP64_OPS[mode])
+    hbm_bytes, ops = n * BYTES_PER_ARC, n * per_q
     t_hbm, t_alu = hbm_bytes / (peaks["hbm_gbs"] * 1e9), ops / (alu_peak * 1e12)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
             traffic = json.load(f).get(f"{mode}:{cfg}:{n}")
+    alu = {"fp64_instr_per_query": per_q,
+           "fp64_instr_source": "ncu (profiles/fp64_sass.json)" if mode in sass else "listing",
+           "algorithmic_ops_per_query": FP64_OPS[mode],
+           "executed_frac": ops / launch_s / 1e12 / alu_peak,
+           "algorithmic_rate_tops": n * FP64_OPS[mode] / launch_s / 1e12,
+           "peak": alu_peak, "unit": "T FP64 instr/s",
+           "peak_source": f"{sms} SM x 64 FP64 lanes x {peaks['sm_max_mhz']:.0f} MHz "
+                          "(tools/fp64_peak.cu measures 18.56 T DADD/s: profiles/r02/)"}
     if t_alu >= t_hbm:
         achieved = ops / launch_s / 1e12
         roof = {"bound": "alu", "achieved": achieved, "peak": alu_peak,
-                "unit": "T FP64 ops/s", "frac": achieved / alu_peak, "traffic": traffic,
-                "peak_source": f"{sms} SM x 64 FP64 lanes x {peaks['sm_max_mhz']:.0f} MHz",
-                "hbm_frac": hbm_bytes / launch_s / 1e9 / peaks["hbm_gbs"]}
+                "unit": "T FP64 instr/s", "frac": achieved / alu_peak, "traffic": traffic,
+                "peak_source": alu["peak_source"],
+                "hbm_frac": hbm_bytes / launch_s / 1e9 / peaks["hbm_gbs"], "alu": alu}
     else:
         achieved = hbm_bytes / launch_s / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                "peak_source": peaks["source"], "alu_frac": ops / launch_s / 1e12 / alu_peak}
+                "traffic_per_query": None if traffic is None else traffic / n,
+                "peak_source": peaks["source"] + " (copy bandwidth)", "alu": alu}
 
     # e2e: the host-buffer C-ABI call, pinned host inputs in, results back to the host
     e2e = None
