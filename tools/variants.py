@@ -17,8 +17,13 @@ OUT = os.path.join(ROOT, "build", "variants")
 
 VARIANTS = {
     "base": {},
-    "fmad_true": {"FMAD": 1},
+    "dbg_fallbacks": {"SGI_DBG_CLOCK": 1},
+    "stages2": {"SGI_EFT_STAGES": 2},
+    "ldg_only": {"SGI_USE_TMA": 0},
+    "ts_knuth": {"SGI_TS_KNUTH": 1},
 }
+if os.environ.get("SGI_VARIANTS"):
+    VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["SGI_VARIANTS"].split(",")}
 
 
 def build():
