@@ -625,6 +625,245 @@ sgi_zonal_emit_warp_kernel(const double* __restrict__ va, const double* __restri
     run_batch_tail<MODE>(W.q[cur], qn, tab, va, vb, lde, cap, out_edge, out_lat, out_count, out_xyz);
 }
 
+// ------------------------------------------------------------------ single-pass fused kernel
+// One launch instead of filter + scan + emit (zonal): persistent CTAs take tiles
+// of kFE consecutive edges in ticket order; per tile the six endpoint planes arrive in shared
+// memory by bulk copies (TMA), the filter writes each edge's candidate range to shared memory,
+// a block scan numbers the tile's pairs, and the tile's output base comes from a decoupled
+// look-back over the preceding tiles' published counts (aggregate / inclusive flags in the
+// workspace; tickets make every earlier tile's CTA resident, so the look-back always
+// completes).  The pairs then run as two-query lanes straight from the staged endpoints and are
+// stored at base + pair index: each edge is read from HBM once and no candidate range leaves
+// the SM.  Pair results are the batch kernel's (same query code).
+#ifndef SGI_ZONAL_FUSED
+#define SGI_ZONAL_FUSED 1
+#endif
+constexpr int kFT = 256;                   // threads per CTA (2 CTAs per SM at <= 128 registers)
+constexpr int kFE = 1024;                  // edges per tile
+constexpr int kFPer = kFE / kFT;           // edges per thread in the filter
+constexpr unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kValMask = (1ull << 62) - 1;
+
+struct FusedSmem {
+  alignas(16) int kcnt[kFE];
+  alignas(16) int excl[kFE + 4];
+  alignas(16) int klo[kFE];
+  int bkt[kBuckets + 1];
+  unsigned wsum[kFT / 32];
+  long long prefix;
+  long long ticket;
+  uint64_t full;
+};
+
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Two pairs' endpoints in the staged tile (lane type W2): coordinate c of edges l0 and l1.
+struct SmemInTwo {
+  uint32_t a0, a1, stride;
+  __device__ __forceinline__ sgi::W2 operator()(int c) const {
+    sgi::W2 v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v.x) : "r"(a0 + (uint32_t)c * stride));
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v.y) : "r"(a1 + (uint32_t)c * stride));
+    return v;
+  }
+};
+
+// The edge of tile pair p: the last e with excl[e] <= p (excl[kFE] = the tile's total).
+__device__ __forceinline__ int pair_edge(const int* excl, int p) {
+  int lo = 0, hi = kFE;                      // excl[lo] <= p < excl[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (excl[mid] <= p) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// Exclusive output base of tile t: warp-wide look-back over the published tile counts.
+__device__ __forceinline__ long long look_back(const unsigned long long* status, int64_t t) {
+  const int lane = threadIdx.x & 31;
+  long long prefix = 0;
+  for (int64_t p = t - 1;; p -= 32) {
+    const int64_t q = p - lane;
+    unsigned long long v = q >= 0 ? ld_acquire_u64(status + q) : kInc;
+    while (__any_sync(0xffffffffu, (v >> 62) == 0)) {
+      if ((v >> 62) == 0) v = ld_acquire_u64(status + q);
+    }
+    const unsigned inc = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+    const int stop = inc ? __ffs(inc) - 1 : 31;
+    long long mine = lane <= stop ? (long long)(v & kValMask) : 0;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, d);
+    prefix += mine;
+    if (inc) break;
+  }
+  return prefix;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kFT, 2)
+sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__ vb, int64_t ne,
+                       int64_t lde, const double* __restrict__ lat, int nlat, int64_t cap,
+                       int64_t* __restrict__ out_edge, int32_t* __restrict__ out_lat,
+                       uint8_t* __restrict__ out_count, double* __restrict__ out_xyz,
+                       unsigned long long* __restrict__ status, unsigned long long* d_total,
+                       bool tma) {
+  extern __shared__ __align__(128) double s_dyn[];
+  __shared__ FusedSmem S;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const size_t lat_words = ((size_t)nlat + 15) / 16 * 16;       // 128-B aligned tile after it
+  double* tab = s_dyn;
+  double* tile = s_dyn + lat_words;                             // [6][kFE]
+  for (int k = tid; k < nlat; k += kFT) tab[k] = lat[k];
+  if (tid == 0) {
+    mbar_init(&S.full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  build_buckets(S.bkt, tab, nlat);
+  const int64_t ntiles = (ne + kFE - 1) / kFE;
+  unsigned long long* ticket_ctr = status + ntiles;
+  auto plane = [&](int c) { return (c < 3 ? va : vb) + (c % 3) * lde; };
+  constexpr bool kW2 = MODE == sgi::MODE_EFT || MODE == sgi::MODE_EFT_LITERAL;
+  uint32_t phase = 0;
+  for (;;) {
+    if (tid == 0) S.ticket = (long long)atomicAdd(ticket_ctr, 1ull);
+    __syncthreads();
+    const int64_t t = S.ticket;
+    if (t >= ntiles) break;
+    const int64_t e0 = t * kFE;
+    const int nv = (int)(ne - e0 < kFE ? ne - e0 : kFE);
+    // ---- endpoints of the tile -> shared memory
+    if (tma && nv == kFE) {
+      if (tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&S.full, 6 * kFE * 8);
+#pragma unroll
+        for (int c = 0; c < 6; ++c) bulk_g2s(tile + c * kFE, plane(c) + e0, kFE * 8, &S.full);
+      }
+      mbar_wait(&S.full, phase);
+      phase ^= 1;
+    } else {
+      for (int i = tid; i < 6 * kFE; i += kFT) {
+        const int c = i / kFE, l = i % kFE;
+        tile[i] = l < nv ? plane(c)[e0 + l] : 0.0;
+      }
+      __syncthreads();
+    }
+    // ---- filter: candidate range of each edge (thread tid: edges tid, tid + kFT, ...)
+#pragma unroll
+    for (int j = 0; j < kFPer; ++j) {
+      const int l = tid + j * kFT;
+      int klo = 0, kcnt = 0;
+      if (l < nv) {
+        double x[6];
+#pragma unroll
+        for (int c = 0; c < 6; ++c) x[c] = tile[c * kFE + l];
+        candidates(x, tab, S.bkt, nlat, klo, kcnt);
+      }
+      S.klo[l] = klo;
+      S.kcnt[l] = kcnt;
+    }
+    __syncthreads();
+    // ---- block scan of the counts (thread tid: edges 4 tid .. 4 tid + 3)
+    const int4 c4 = *reinterpret_cast<const int4*>(&S.kcnt[kFPer * tid]);
+    const unsigned mine = (unsigned)(c4.x + c4.y + c4.z + c4.w);
+    unsigned incl = mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += y;
+    }
+    if (lane == 31) S.wsum[warp] = incl;
+    __syncthreads();
+    unsigned before = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < kFT / 32; ++w) {
+      const unsigned x = S.wsum[w];
+      before += w < warp ? x : 0;
+      total += x;
+    }
+    {
+      const int b = (int)(before + incl - mine);
+      *reinterpret_cast<int4*>(&S.excl[kFPer * tid]) =
+          make_int4(b, b + c4.x, b + c4.x + c4.y, b + c4.x + c4.y + c4.z);
+      if (tid == kFT - 1) S.excl[kFE] = (int)total;
+    }
+    // publish this tile's count (its aggregate; tile 0's is already inclusive)
+    if (tid == 0) st_release_u64(status + t, (t == 0 ? kInc : kAgg) | (unsigned long long)total);
+    __syncthreads();
+    const int T = (int)total;
+    // ---- the tile's pairs, 2 kFT per round (two per thread); the output base is needed only
+    // at the first store, so the look-back runs after the first round's arithmetic
+    bool have_prefix = false;
+    for (int r0 = 0; r0 < T || !have_prefix; r0 += 2 * kFT) {
+      const int p0 = r0 + tid, p1 = r0 + kFT + tid;
+      const bool v0 = p0 < T, v1 = p1 < T;
+      sgi::QueryOut o[2];
+      bool ok[2] = {true, true};
+      int le[2] = {0, 0}, kk[2] = {0, 0};
+      double zz[2] = {0.0, 0.0};
+      if (v0) {
+        le[0] = pair_edge(S.excl, p0);
+        kk[0] = S.klo[le[0]] + (p0 - S.excl[le[0]]);
+        le[1] = le[0];
+        kk[1] = kk[0];
+        if (v1) {
+          le[1] = pair_edge(S.excl, p1);
+          kk[1] = S.klo[le[1]] + (p1 - S.excl[le[1]]);
+        }
+        zz[0] = tab[kk[0]];
+        zz[1] = tab[kk[1]];
+        if constexpr (kW2) {
+          const SmemInTwo in = {smem_u32(tile + le[0]), smem_u32(tile + le[1]), kFE * 8};
+          sgi::QueryOut2 q;
+          const sgi::B2 okb = sgi::query_fast2<MODE>(in, sgi::W2{zz[0], zz[1]}, q);
+          o[0] = {q.p0x.x, q.p0y.x, q.p1x.x, q.p1y.x, q.count[0]};
+          o[1] = {q.p0x.y, q.p0y.y, q.p1x.y, q.p1y.y, q.count[1]};
+          ok[0] = okb.x;
+          ok[1] = okb.y;
+        } else {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (h == 1 && !v1) break;
+            const sgi::SmemIn in = {smem_u32(tile + le[h]), kFE * 8};
+            ok[h] = sgi::query_fast<MODE>(in, zz[h], o[h]);
+          }
+        }
+      }
+      if (!have_prefix) {
+        if (warp == 0) {
+          const long long pre = t == 0 ? 0 : look_back(status, t);
+          if (lane == 0) {
+            if (t > 0) st_release_u64(status + t, kInc | (unsigned long long)(pre + T));
+            S.prefix = pre;
+            if (t == ntiles - 1) *d_total = (unsigned long long)(pre + T);
+          }
+        }
+        __syncthreads();
+        have_prefix = true;
+      }
+      const long long base = S.prefix;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (!(h == 0 ? v0 : v1)) continue;
+        const int64_t j = base + (h == 0 ? p0 : p1);
+        if (j >= cap) continue;
+        if (ok[h]) store_pair(o[h], zz[h], e0 + le[h], kk[h], j, cap, out_edge, out_lat, out_count,
+                              out_xyz);
+        else emit_exact<MODE>(va, vb, lde, tab, e0 + le[h], kk[h], j, cap, out_edge, out_lat,
+                              out_count, out_xyz);
+      }
+    }
+    __syncthreads();                   // the tile buffer and S are reused by the next tile
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -680,6 +919,43 @@ sgi_status sgi_zonal_intersect(const double* va, const double* vb, int64_t n_edg
     return (int)(g < ntiles ? g : ntiles);
   };
   const bool smem_tab = n_lat <= kLatSmem;
+  const int64_t ntiles_f = (n_edges + kFE - 1) / kFE;
+  const bool fused = SGI_ZONAL_FUSED && cap > 0 && smem_tab &&
+                     work_bytes >= (size_t)(ntiles_f + 1) * sizeof(unsigned long long);
+  if (fused) {
+    // status words of the tiles and the ticket counter, zeroed for this call
+    unsigned long long* status = (unsigned long long*)d_work;
+    e = cudaMemsetAsync(status, 0, (size_t)(ntiles_f + 1) * sizeof(unsigned long long), st);
+    if (e != cudaSuccess) {
+      sgi_internal::set_error_msg("sgi_zonal_intersect: cudaMemsetAsync", e);
+      return SGI_E_CUDA;
+    }
+    const bool tma = ((((uintptr_t)va | (uintptr_t)vb) & 15) == 0) && (ld_e % 2 == 0);
+    const size_t smem = ((size_t)n_lat + 15) / 16 * 16 * sizeof(double) + 6 * kFE * sizeof(double);
+    auto fk = [&](auto kernel) {
+      int occ = 1;
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kFT, smem);
+      const int64_t g = (int64_t)sms * (occ < 1 ? 1 : occ);
+      kernel<<<(int)(g < ntiles_f ? g : ntiles_f), kFT, smem, st>>>(
+          va, vb, n_edges, ld_e, lat_z0, n_lat, cap, out_edge, out_lat, out_count, out_xyz, status,
+          d_total, tma);
+    };
+    switch (mode) {
+      case SGI_MODE_NAIVE: fk(sgi_zonal_fused_kernel<sgi::MODE_NAIVE>); break;
+      case SGI_MODE_EFT: fk(sgi_zonal_fused_kernel<sgi::MODE_EFT>); break;
+      case SGI_MODE_EFT_LITERAL: fk(sgi_zonal_fused_kernel<sgi::MODE_EFT_LITERAL>); break;
+      case SGI_MODE_YAC: fk(sgi_zonal_fused_kernel<sgi::MODE_YAC>); break;
+      case SGI_MODE_BASE: fk(sgi_zonal_fused_kernel<sgi::MODE_BASE>); break;
+      default: fk(sgi_zonal_fused_kernel<sgi::MODE_NAIVE_KAHAN>); break;
+    }
+    e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      sgi_internal::set_error_msg("sgi_zonal_fused_kernel launch", e);
+      return SGI_E_CUDA;
+    }
+    return SGI_OK;
+  }
   const size_t filter_smem = (SGI_ZONAL_FILTER_PREFETCH == 2 ? lat_smem_even : lat_smem) +
                              (SGI_ZONAL_FILTER_PREFETCH == 2 ? 2 * 6 * kEdges * sizeof(double) : 0);
   if (smem_tab) {
