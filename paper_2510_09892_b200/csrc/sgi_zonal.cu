@@ -654,12 +654,15 @@ struct FusedSmem {
   uint64_t full;
 };
 
-__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// A tile's status word carries all that is published (flag and count in one aligned 64-bit
+// word, single-copy atomic), so relaxed GPU-scope accesses suffice: no other data is ordered
+// by it.  (Acquire loads would invalidate L1 — CCTL.IVALL — on every poll.)
+__device__ __forceinline__ void st_status(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+__device__ __forceinline__ unsigned long long ld_status(const unsigned long long* p) {
   unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 
@@ -684,23 +687,47 @@ __device__ __forceinline__ int pair_edge(const int* excl, int p) {
   return lo;
 }
 
-// Exclusive output base of tile t: warp-wide look-back over the published tile counts.
+// Exclusive output base of tile t: warp-wide look-back over the published tile counts, four
+// tiles per lane per step (128 tiles per L2 round trip).
 __device__ __forceinline__ long long look_back(const unsigned long long* status, int64_t t) {
   const int lane = threadIdx.x & 31;
   long long prefix = 0;
-  for (int64_t p = t - 1;; p -= 32) {
-    const int64_t q = p - lane;
-    unsigned long long v = q >= 0 ? ld_acquire_u64(status + q) : kInc;
-    while (__any_sync(0xffffffffu, (v >> 62) == 0)) {
-      if ((v >> 62) == 0) v = ld_acquire_u64(status + q);
+  for (int64_t p = t - 1;; p -= 128) {
+    unsigned long long v[4];
+    bool stop_here = false;
+    long long mine = 0;
+    // lane L covers tiles p - 4L .. p - 4L - 3 (nearest first)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t q = p - 4 * lane - j;
+      v[j] = q >= 0 ? ld_status(status + q) : kInc;
     }
-    const unsigned inc = __ballot_sync(0xffffffffu, (v >> 62) == 2);
-    const int stop = inc ? __ffs(inc) - 1 : 31;
-    long long mine = lane <= stop ? (long long)(v & kValMask) : 0;
+    for (;;) {
+      bool missing = false;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) missing |= (v[j] >> 62) == 0;
+      if (!__any_sync(0xffffffffu, missing)) break;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t q = p - 4 * lane - j;
+        if ((v[j] >> 62) == 0) v[j] = ld_status(status + q);
+      }
+    }
+    // the nearest inclusive entry (lowest lane, then lowest j) ends the walk
+    int jinc = 4;
+#pragma unroll
+    for (int j = 3; j >= 0; --j)
+      if ((v[j] >> 62) == 2) jinc = j;
+    const unsigned inc = __ballot_sync(0xffffffffu, jinc < 4);
+    const int first = inc ? __ffs(inc) - 1 : 32;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (lane < first || (lane == first && j <= jinc)) mine += (long long)(v[j] & kValMask);
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, d);
     prefix += mine;
-    if (inc) break;
+    stop_here = inc != 0;
+    if (stop_here) break;
   }
   return prefix;
 }
@@ -795,7 +822,7 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
       if (tid == kFT - 1) S.excl[kFE] = (int)total;
     }
     // publish this tile's count (its aggregate; tile 0's is already inclusive)
-    if (tid == 0) st_release_u64(status + t, (t == 0 ? kInc : kAgg) | (unsigned long long)total);
+    if (tid == 0) st_status(status + t, (t == 0 ? kInc : kAgg) | (unsigned long long)total);
     __syncthreads();
     const int T = (int)total;
     // ---- the tile's pairs, 2 kFT per round (two per thread); the output base is needed only
@@ -840,7 +867,7 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
         if (warp == 0) {
           const long long pre = t == 0 ? 0 : look_back(status, t);
           if (lane == 0) {
-            if (t > 0) st_release_u64(status + t, kInc | (unsigned long long)(pre + T));
+            if (t > 0) st_status(status + t, kInc | (unsigned long long)(pre + T));
             S.prefix = pre;
             if (t == ntiles - 1) *d_total = (unsigned long long)(pre + T);
           }
