@@ -53,3 +53,25 @@ def build_devtests(force: bool = False) -> str:
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
     return DEVTEST_LIB
+
+
+DEBUG_LIB = os.path.join(ROOT, "build", "debug", "libsgi_debug.so")
+
+
+def build_debug(force: bool = False) -> str:
+    """Test-only variant of libsgi.so with device-side checks (-DSGI_DEBUG_CHECKS=1: asserts on
+    every queue / table / tile index, poisoned shared scratch; csrc/sgi_tma.cuh) — the stand-in
+    for compute-sanitizer, which this GPU pool does not run."""
+    srcs = sources()
+    if (not force and os.path.exists(DEBUG_LIB)
+            and all(os.path.getmtime(DEBUG_LIB) >= os.path.getmtime(s) for s in srcs)):
+        return DEBUG_LIB
+    os.makedirs(os.path.dirname(DEBUG_LIB), exist_ok=True)
+    cu = [s for s in srcs if s.endswith(".cu")]
+    flags = [f for f in NVCC_FLAGS if f not in ("-Xptxas", "-v")]
+    cmd = ["nvcc", *flags, "-DSGI_DEBUG_CHECKS=1", "-I", os.path.join(ROOT, "include"), "-o",
+           DEBUG_LIB, *cu]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
+    return DEBUG_LIB

@@ -2,7 +2,23 @@
 // (sgi_capi.cu: the query kernels).  Inline PTX for sm_100a:
 // cp.async.bulk global -> shared with an mbarrier counting the bytes (UBLKCP in SASS).
 #pragma once
+#include <cassert>
 #include <cstdint>
+
+// Debug builds (-DSGI_DEBUG_CHECKS=1; tests/test_gpu_debug_checks.py) stand in for
+// compute-sanitizer, which this pool does not run: device asserts on every shared-memory queue
+// index, table index and tile index the kernels form, and shared scratch poisoned (all bits set:
+// NaN doubles, -1 indices) at kernel start so a read of a slot nobody wrote shows up as a failed
+// assert or a changed result.  Release builds compile both to nothing.
+#ifndef SGI_DEBUG_CHECKS
+#define SGI_DEBUG_CHECKS 0
+#endif
+#if SGI_DEBUG_CHECKS
+#undef NDEBUG
+#define SGI_CHECK(c) assert(c)
+#else
+#define SGI_CHECK(c) ((void)0)
+#endif
 
 namespace {
 
@@ -45,4 +61,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 
+}  // namespace
+
+namespace {
+// Debug builds: fill `bytes` of shared memory at p with 0xFF (cooperatively, all threads).
+__device__ __forceinline__ void sgi_poison_smem(void* p, size_t bytes) {
+#if SGI_DEBUG_CHECKS
+  unsigned char* c = static_cast<unsigned char*>(p);
+  for (size_t i = threadIdx.x; i < bytes; i += blockDim.x) c[i] = 0xFF;
+#else
+  (void)p;
+  (void)bytes;
+#endif
+}
 }  // namespace

@@ -433,8 +433,10 @@ __device__ __forceinline__ void run_batch(const WarpQueue& q, int n, const doubl
                                           uint8_t* __restrict__ out_count,
                                           double* __restrict__ out_xyz) {
   const int lane = threadIdx.x & 31;
+  SGI_CHECK(n >= 0 && n <= kBatch);
   auto store = [&](const sgi::QueryOut& o, double z0, bool ok, int r) {
     if (r >= n) return;
+    SGI_CHECK(q.lat[r] >= 0 && q.slot[r] >= 0 && q.edge[r] >= 0);
     const int64_t j = q.slot[r];
     if (j >= cap) return;
     if (ok) store_pair(o, z0, q.edge[r], q.lat[r], j, cap, out_edge, out_lat, out_count, out_xyz);
@@ -490,6 +492,11 @@ sgi_zonal_emit_warp_kernel(const double* __restrict__ va, const double* __restri
   const double* tab = SMEM ? s_dyn : lat;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpSmem& W = reinterpret_cast<WarpSmem*>(s_dyn + lat_words)[warp];
+#if SGI_DEBUG_CHECKS
+  if (SMEM) __syncthreads();      // the table copy is complete before the scratch is poisoned
+  sgi_poison_smem(reinterpret_cast<WarpSmem*>(s_dyn + lat_words), kWarpsPerCta * sizeof(WarpSmem));
+  __syncthreads();
+#endif
   // this warp's tiles t0, t0 + nwarps, ... (grid stride: at any time the warps of the grid
   // work on neighbouring tiles, which measured faster than contiguous per-warp ranges)
   const int64_t ntiles = (ne + kEdges - 1) / kEdges;
@@ -700,6 +707,7 @@ __device__ __forceinline__ long long look_back(const unsigned long long* status,
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int64_t q = p - 4 * lane - j;
+      SGI_CHECK(q < t);
       v[j] = q >= 0 ? ld_status(status + q) : kInc;
     }
     for (;;) {
@@ -746,6 +754,9 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
   const size_t lat_words = ((size_t)nlat + 15) / 16 * 16;       // 128-B aligned tile after it
   double* tab = s_dyn;
   double* tile = s_dyn + lat_words;                             // [6][kFE]
+  sgi_poison_smem(&S, sizeof(S));
+  sgi_poison_smem(s_dyn + lat_words, 6 * kFE * sizeof(double));
+  __syncthreads();
   for (int k = tid; k < nlat; k += kFT) tab[k] = lat[k];
   if (tid == 0) {
     mbar_init(&S.full, 1);
@@ -836,6 +847,7 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
       int le[2] = {0, 0}, kk[2] = {0, 0};
       double zz[2] = {0.0, 0.0};
       if (v0) {
+        SGI_CHECK(S.excl[0] == 0 && S.excl[kFE] == T);
         le[0] = pair_edge(S.excl, p0);
         kk[0] = S.klo[le[0]] + (p0 - S.excl[le[0]]);
         le[1] = le[0];
@@ -844,6 +856,9 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
           le[1] = pair_edge(S.excl, p1);
           kk[1] = S.klo[le[1]] + (p1 - S.excl[le[1]]);
         }
+        SGI_CHECK(le[0] >= 0 && le[0] < nv && le[1] >= 0 && le[1] < nv);
+        SGI_CHECK(kk[0] >= 0 && kk[0] < nlat && kk[1] >= 0 && kk[1] < nlat);
+        SGI_CHECK(p0 >= S.excl[le[0]] && p0 < S.excl[le[0] + 1]);
         zz[0] = tab[kk[0]];
         zz[1] = tab[kk[1]];
         if constexpr (kW2) {
