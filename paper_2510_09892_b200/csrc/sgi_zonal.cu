@@ -645,6 +645,9 @@ sgi_zonal_emit_warp_kernel(const double* __restrict__ va, const double* __restri
 #ifndef SGI_ZONAL_FUSED
 #define SGI_ZONAL_FUSED 1
 #endif
+#ifndef SGI_ZONAL_STATIC
+#define SGI_ZONAL_STATIC 1
+#endif
 constexpr int kFT = 256;                   // threads per CTA (2 CTAs per SM at <= 128 registers)
 constexpr int kFE = 1024;                  // edges per tile
 constexpr int kFPer = kFE / kFT;           // edges per thread in the filter
@@ -769,11 +772,19 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
   auto plane = [&](int c) { return (c < 3 ? va : vb) + (c % 3) * lde; };
   constexpr bool kW2 = MODE == sgi::MODE_EFT || MODE == sgi::MODE_EFT_LITERAL;
   uint32_t phase = 0;
+#if SGI_ZONAL_STATIC
+  // static assignment (tiles blockIdx.x, + gridDim.x, ...): the cooperative launch makes every
+  // CTA resident, so every earlier tile's CTA runs and the look-back completes; each CTA knows
+  // its next tile and prefetches it into L2 under the current tile's arithmetic
+  (void)ticket_ctr;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+#else
   for (;;) {
     if (tid == 0) S.ticket = (long long)atomicAdd(ticket_ctr, 1ull);
     __syncthreads();
     const int64_t t = S.ticket;
     if (t >= ntiles) break;
+#endif
     const int64_t e0 = t * kFE;
     const int nv = (int)(ne - e0 < kFE ? ne - e0 : kFE);
     // ---- endpoints of the tile -> shared memory
@@ -808,6 +819,14 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
       S.kcnt[l] = kcnt;
     }
     __syncthreads();
+#if SGI_ZONAL_STATIC
+    if (tid == 0 && tma && t + gridDim.x < ntiles && ne - (t + gridDim.x) * kFE >= kFE) {
+#pragma unroll
+      for (int c = 0; c < 6; ++c)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(plane(c) + (t + gridDim.x) * kFE),
+                     "r"(kFE * 8) : "memory");
+    }
+#endif
     // ---- block scan of the counts (thread tid: edges 4 tid .. 4 tid + 3)
     const int4 c4 = *reinterpret_cast<const int4*>(&S.kcnt[kFPer * tid]);
     const unsigned mine = (unsigned)(c4.x + c4.y + c4.z + c4.w);
@@ -979,9 +998,25 @@ sgi_status sgi_zonal_intersect(const double* va, const double* vb, int64_t n_edg
       cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kFT, smem);
       const int64_t g = (int64_t)sms * (occ < 1 ? 1 : occ);
-      kernel<<<(int)(g < ntiles_f ? g : ntiles_f), kFT, smem, st>>>(
-          va, vb, n_edges, ld_e, lat_z0, n_lat, cap, out_edge, out_lat, out_count, out_xyz, status,
-          d_total, tma);
+      const int grid = (int)(g < ntiles_f ? g : ntiles_f);
+#if SGI_ZONAL_STATIC
+      // cooperative launch: all CTAs co-resident (the static look-back relies on it)
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(kFT);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeCooperative;
+      attr[0].val.cooperative = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      e = cudaLaunchKernelEx(&cfg, kernel, va, vb, n_edges, ld_e, lat_z0, (int)n_lat, cap, out_edge,
+                             out_lat, out_count, out_xyz, status, d_total, tma);
+#else
+      kernel<<<grid, kFT, smem, st>>>(va, vb, n_edges, ld_e, lat_z0, n_lat, cap, out_edge, out_lat,
+                                      out_count, out_xyz, status, d_total, tma);
+#endif
     };
     switch (mode) {
       case SGI_MODE_NAIVE: fk(sgi_zonal_fused_kernel<sgi::MODE_NAIVE>); break;
