@@ -646,11 +646,12 @@ sgi_zonal_emit_warp_kernel(const double* __restrict__ va, const double* __restri
 #define SGI_ZONAL_FUSED 1
 #endif
 #ifndef SGI_ZONAL_STATIC
-#define SGI_ZONAL_STATIC 1
+#define SGI_ZONAL_STATIC 0   // 1: static tiles + cooperative launch (0.478 ms vs 0.44: look-back waits)
 #endif
 constexpr int kFT = 256;                   // threads per CTA (2 CTAs per SM at <= 128 registers)
 constexpr int kFE = 1024;                  // edges per tile
 constexpr int kFPer = kFE / kFT;           // edges per thread in the filter
+constexpr int kFP = 2 * kFT;               // pairs per round (two per thread)
 constexpr unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kValMask = (1ull << 62) - 1;
 
 struct FusedSmem {
@@ -772,6 +773,43 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
   auto plane = [&](int c) { return (c < 3 ? va : vb) + (c % 3) * lde; };
   constexpr bool kW2 = MODE == sgi::MODE_EFT || MODE == sgi::MODE_EFT_LITERAL;
   uint32_t phase = 0;
+  // parked results of the previous one-round tile: 4 coordinates per pair slot + packed
+  // (edge in tile, latitude, count, ok, valid)
+  double* park = tile + 6 * kFE;                                // [4][kFP]
+  unsigned* park_meta = reinterpret_cast<unsigned*>(park + 4 * kFP);
+  int64_t prev_t = 0;
+  int prev_T = 0;
+  bool have_prev = false;
+  // look back for the parked tile, publish its inclusive count, store its results
+  auto flush_parked = [&]() {
+    if (warp == 0) {
+      const long long pre = prev_t == 0 ? 0 : look_back(status, prev_t);
+      if (lane == 0) {
+        if (prev_t > 0) st_status(status + prev_t, kInc | (unsigned long long)(pre + prev_T));
+        S.prefix = pre;
+        if (prev_t == ntiles - 1) *d_total = (unsigned long long)(pre + prev_T);
+      }
+    }
+    __syncthreads();
+    const long long base = S.prefix;
+    const int64_t pe0 = prev_t * kFE;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int sl = h * kFT + tid;
+      const unsigned m = park_meta[sl];
+      if (!(m >> 31)) continue;
+      const int64_t j = base + sl;
+      if (j >= cap) continue;
+      const int le = (int)(m & 1023u), kk = (int)((m >> 10) & 4095u);
+      const sgi::QueryOut o = {park[0 * kFP + sl], park[1 * kFP + sl], park[2 * kFP + sl],
+                               park[3 * kFP + sl], (uint8_t)((m >> 22) & 255u)};
+      if ((m >> 30) & 1u) store_pair(o, tab[kk], pe0 + le, kk, j, cap, out_edge, out_lat,
+                                     out_count, out_xyz);
+      else emit_exact<MODE>(va, vb, lde, tab, pe0 + le, kk, j, cap, out_edge, out_lat, out_count,
+                            out_xyz);
+    }
+    __syncthreads();                   // S.prefix and the parked slots are free again
+  };
 #if SGI_ZONAL_STATIC
   // static assignment (tiles blockIdx.x, + gridDim.x, ...): the cooperative launch makes every
   // CTA resident, so every earlier tile's CTA runs and the look-back completes; each CTA knows
@@ -819,14 +857,14 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
       S.kcnt[l] = kcnt;
     }
     __syncthreads();
-#if SGI_ZONAL_STATIC
+    // tile t + gridDim.x (about the ticket some CTA draws next) into L2 under this tile's
+    // arithmetic, so that CTA's bulk copies hit L2
     if (tid == 0 && tma && t + gridDim.x < ntiles && ne - (t + gridDim.x) * kFE >= kFE) {
 #pragma unroll
       for (int c = 0; c < 6; ++c)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(plane(c) + (t + gridDim.x) * kFE),
                      "r"(kFE * 8) : "memory");
     }
-#endif
     // ---- block scan of the counts (thread tid: edges 4 tid .. 4 tid + 3)
     const int4 c4 = *reinterpret_cast<const int4*>(&S.kcnt[kFPer * tid]);
     const unsigned mine = (unsigned)(c4.x + c4.y + c4.z + c4.w);
@@ -855,10 +893,18 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
     if (tid == 0) st_status(status + t, (t == 0 ? kInc : kAgg) | (unsigned long long)total);
     __syncthreads();
     const int T = (int)total;
-    // ---- the tile's pairs, 2 kFT per round (two per thread); the output base is needed only
-    // at the first store, so the look-back runs after the first round's arithmetic
-    bool have_prefix = false;
-    for (int r0 = 0; r0 < T || !have_prefix; r0 += 2 * kFT) {
+    // ---- the tile's pairs, 2 kFT per round (thread tid: pairs r0 + tid, r0 + kFT + tid).  A
+    // one-round tile (the usual case) parks its results in shared memory and stores them one tile
+    // later, after the look-back for it — by then its predecessors have long published, so the
+    // look-back is one L2 round trip instead of a wait; a larger tile flushes the parked one and
+    // stores at once.
+    const bool multi = T > 2 * kFT;
+    if (multi && have_prev) {
+      flush_parked();
+      have_prev = false;
+    }
+    bool have_prefix = !multi;
+    for (int r0 = 0; r0 < T || !have_prefix || r0 == 0; r0 += 2 * kFT) {
       const int p0 = r0 + tid, p1 = r0 + kFT + tid;
       const bool v0 = p0 < T, v1 = p1 < T;
       sgi::QueryOut o[2];
@@ -897,6 +943,24 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
           }
         }
       }
+      if (!multi) {
+        // store the parked tile (look-back for it first), then park this one
+        if (have_prev) flush_parked();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int sl = h * kFT + tid;
+          park[0 * kFP + sl] = o[h].p0x;
+          park[1 * kFP + sl] = o[h].p0y;
+          park[2 * kFP + sl] = o[h].p1x;
+          park[3 * kFP + sl] = o[h].p1y;
+          park_meta[sl] = (unsigned)le[h] | ((unsigned)kk[h] << 10) | ((unsigned)o[h].count << 22) |
+                          ((unsigned)ok[h] << 30) | ((unsigned)(h == 0 ? v0 : v1) << 31);
+        }
+        prev_t = t;
+        prev_T = T;
+        have_prev = true;
+        break;
+      }
       if (!have_prefix) {
         if (warp == 0) {
           const long long pre = t == 0 ? 0 : look_back(status, t);
@@ -923,6 +987,7 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
     }
     __syncthreads();                   // the tile buffer and S are reused by the next tile
   }
+  if (have_prev) flush_parked();
 }
 
 }  // namespace
@@ -992,7 +1057,8 @@ sgi_status sgi_zonal_intersect(const double* va, const double* vb, int64_t n_edg
       return SGI_E_CUDA;
     }
     const bool tma = ((((uintptr_t)va | (uintptr_t)vb) & 15) == 0) && (ld_e % 2 == 0);
-    const size_t smem = ((size_t)n_lat + 15) / 16 * 16 * sizeof(double) + 6 * kFE * sizeof(double);
+    const size_t smem = ((size_t)n_lat + 15) / 16 * 16 * sizeof(double) +
+                        (6 * kFE + 4 * kFP) * sizeof(double) + kFP * sizeof(unsigned);
     auto fk = [&](auto kernel) {
       int occ = 1;
       cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
