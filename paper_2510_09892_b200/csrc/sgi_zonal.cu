@@ -144,7 +144,9 @@ __device__ __forceinline__ void candidates(const double* x, const double* tab, c
   const double za = __dmul_rn(x[2], fast_rsqrt(ra2)), zb = __dmul_rn(x[5], fast_rsqrt(rb2));
   const double g1 = __dsub_rn(__dmul_rn(nx, x[1]), __dmul_rn(ny, x[0]));
   const double g2 = __dsub_rn(__dmul_rn(nx, x[4]), __dmul_rn(ny, x[3]));
-  double zhi = fmax(za, zb), zlo = fmin(za, zb);
+  const bool zbig = zb > za;                         // (NaN inputs are screened below)
+  double zhi = zbig ? zb : za, zlo = zbig ? za : zb;
+  const bool finite = za == za && zb == zb;
   const bool top_inside = g1 > 0.0 && g2 < 0.0, bottom_inside = g1 < 0.0 && g2 > 0.0;
   if (top_inside || bottom_inside) {                 // the circle's extremum is on the arc
     const double s2 = __dadd_rn(__dmul_rn(nx, nx), __dmul_rn(ny, ny));
@@ -155,7 +157,7 @@ __device__ __forceinline__ void candidates(const double* x, const double* tab, c
   }
   if (nx == 0.0 && ny == 0.0 && nz == 0.0) {
     kcnt = nlat;                                     // n = 0: degenerate at every latitude
-  } else if (zhi == zhi && zlo == zlo) {             // NaN inputs: no candidates
+  } else if (finite && zhi == zhi && zlo == zlo) {   // NaN inputs: no candidates
     klo = bucket_search<false>(bkt, tab, nlat, __dsub_rn(zlo, kDelta));
     // first k with tab[k] > zhi + delta: mesh edges span a latitude or two, so step from klo
     // and search only past kStep entries (the same index either way)
@@ -821,8 +823,10 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
   (void)ticket_ctr;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
 #else
+  // the first ticket here; each later one is drawn while the previous tile's results are being
+  // stored, so its atomic round trip is off the critical path
+  if (tid == 0) S.ticket = (long long)atomicAdd(ticket_ctr, 1ull);
   for (;;) {
-    if (tid == 0) S.ticket = (long long)atomicAdd(ticket_ctr, 1ull);
     __syncthreads();
     const int64_t t = S.ticket;
     if (t >= ntiles) break;
@@ -897,8 +901,13 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
       int o = b;
 #pragma unroll
       for (int j = 0; j < kFPer; ++j) {
-        const int stop = min(o + cs[j], kFP);
-        for (int q = o; q < stop; ++q) S.pmap[q] = (unsigned short)(kFPer * tid + j);
+        const unsigned short e = (unsigned short)(kFPer * tid + j);
+        if (cs[j] == 1) {                            // the usual case: one latitude
+          if (o < kFP) S.pmap[o] = e;
+        } else if (cs[j] > 1) {
+          const int stop = min(o + cs[j], kFP);
+          for (int q = o; q < stop; ++q) S.pmap[q] = e;
+        }
         o += cs[j];
       }
     }
@@ -972,6 +981,9 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
         prev_t = t;
         prev_T = T;
         have_prev = true;
+#if !SGI_ZONAL_STATIC
+        if (tid == 0) S.ticket = (long long)atomicAdd(ticket_ctr, 1ull);
+#endif
         break;
       }
       if (!have_prefix) {
@@ -987,6 +999,9 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
         have_prefix = true;
       }
       const long long base = S.prefix;
+#if !SGI_ZONAL_STATIC
+      if (tid == 0 && r0 + 2 * kFT >= T) S.ticket = (long long)atomicAdd(ticket_ctr, 1ull);
+#endif
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         if (!(h == 0 ? v0 : v1)) continue;
