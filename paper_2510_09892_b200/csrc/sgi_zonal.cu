@@ -705,31 +705,20 @@ __device__ __forceinline__ int pair_edge(const int* excl, int p) {
 }
 
 // Exclusive output base of tile t: warp-wide look-back over the published tile counts, four
-// tiles per lane per step (128 tiles per L2 round trip).  The first window's status words are
-// polled early (look_back_poll, before the warp's own arithmetic) and passed in: an entry seen as
-// an aggregate is still correct, a missing one is polled again.
-__device__ __forceinline__ void look_back_poll(const unsigned long long* status, int64_t t,
-                                               unsigned long long (&v)[4]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int64_t q = t - 1 - 4 * lane - j;
-    SGI_CHECK(q < t);
-    v[j] = q >= 0 ? ld_status(status + q) : kInc;
-  }
-}
-
-__device__ __forceinline__ long long look_back(const unsigned long long* status, int64_t t,
-                                               unsigned long long (&v)[4]) {
+// tiles per lane per step (128 tiles per L2 round trip).
+__device__ __forceinline__ long long look_back(const unsigned long long* status, int64_t t) {
   const int lane = threadIdx.x & 31;
   long long prefix = 0;
   for (int64_t p = t - 1;; p -= 128) {
-    if (p != t - 1) {
+    unsigned long long v[4];
+    bool stop_here = false;
+    long long mine = 0;
+    // lane L covers tiles p - 4L .. p - 4L - 3 (nearest first)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t q = p - 4 * lane - j;
-        v[j] = q >= 0 ? ld_status(status + q) : kInc;
-      }
+    for (int j = 0; j < 4; ++j) {
+      const int64_t q = p - 4 * lane - j;
+      SGI_CHECK(q < t);
+      v[j] = q >= 0 ? ld_status(status + q) : kInc;
     }
     for (;;) {
       bool missing = false;
@@ -749,14 +738,14 @@ __device__ __forceinline__ long long look_back(const unsigned long long* status,
       if ((v[j] >> 62) == 2) jinc = j;
     const unsigned inc = __ballot_sync(0xffffffffu, jinc < 4);
     const int first = inc ? __ffs(inc) - 1 : 32;
-    long long mine = 0;
 #pragma unroll
     for (int j = 0; j < 4; ++j)
       if (lane < first || (lane == first && j <= jinc)) mine += (long long)(v[j] & kValMask);
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, d);
     prefix += mine;
-    if (inc) break;
+    stop_here = inc != 0;
+    if (stop_here) break;
   }
   return prefix;
 }
@@ -800,9 +789,7 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
   // look back for the parked tile, publish its inclusive count, store its results
   auto flush_parked = [&]() {
     if (warp == 0) {
-      unsigned long long lbp[4];
-      look_back_poll(status, prev_t, lbp);
-      const long long pre = prev_t == 0 ? 0 : look_back(status, prev_t, lbp);
+      const long long pre = prev_t == 0 ? 0 : look_back(status, prev_t);
       if (lane == 0) {
         if (prev_t > 0) st_status(status + prev_t, kInc | (unsigned long long)(pre + prev_T));
         S.prefix = pre;
@@ -939,8 +926,6 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
       have_prev = false;
     }
     bool have_prefix = !multi;
-    unsigned long long lbv[4] = {kInc, kInc, kInc, kInc};
-    if (!have_prefix && warp == 0) look_back_poll(status, t, lbv);
     for (int r0 = 0; r0 < T || !have_prefix || r0 == 0; r0 += 2 * kFT) {
       const int p0 = r0 + tid, p1 = r0 + kFT + tid;
       const bool v0 = p0 < T, v1 = p1 < T;
@@ -1003,7 +988,7 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
       }
       if (!have_prefix) {
         if (warp == 0) {
-          const long long pre = t == 0 ? 0 : look_back(status, t, lbv);
+          const long long pre = t == 0 ? 0 : look_back(status, t);
           if (lane == 0) {
             if (t > 0) st_status(status + t, kInc | (unsigned long long)(pre + T));
             S.prefix = pre;
