@@ -653,8 +653,12 @@ sgi_zonal_emit_warp_kernel(const double* __restrict__ va, const double* __restri
 #ifndef SGI_ZONAL_STATIC
 #define SGI_ZONAL_STATIC 0   // 1: static tiles + cooperative launch (0.478 ms vs 0.44: look-back waits)
 #endif
-constexpr int kFT = 256;                   // threads per CTA (2 CTAs per SM at <= 128 registers)
-constexpr int kFE = 1024;                  // edges per tile
+#ifndef SGI_ZONAL_FT
+#define SGI_ZONAL_FT 256
+#endif
+constexpr int kFT = SGI_ZONAL_FT;          // threads per CTA (256: 2 CTAs per SM at <= 128 registers)
+constexpr int kFE = 4 * kFT;               // edges per tile
+constexpr int kFMinB = kFT <= 256 ? 2 : 1;
 constexpr int kFPer = kFE / kFT;           // edges per thread in the filter
 constexpr int kFP = 2 * kFT;               // pairs per round (two per thread)
 constexpr unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kValMask = (1ull << 62) - 1;
@@ -751,21 +755,21 @@ __device__ __forceinline__ long long look_back(const unsigned long long* status,
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kFT, 2)
+__global__ void __launch_bounds__(kFT, kFMinB)
 sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__ vb, int64_t ne,
                        int64_t lde, const double* __restrict__ lat, int nlat, int64_t cap,
                        int64_t* __restrict__ out_edge, int32_t* __restrict__ out_lat,
                        uint8_t* __restrict__ out_count, double* __restrict__ out_xyz,
                        unsigned long long* __restrict__ status, unsigned long long* d_total,
                        bool tma) {
-  extern __shared__ __align__(128) double s_dyn[];
+  extern __shared__ __align__(128) double s_fused[];
   __shared__ FusedSmem S;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const size_t lat_words = ((size_t)nlat + 15) / 16 * 16;       // 128-B aligned tile after it
-  double* tab = s_dyn;
-  double* tile = s_dyn + lat_words;                             // [6][kFE]
+  double* tab = s_fused;
+  double* tile = s_fused + lat_words;                             // [6][kFE]
   sgi_poison_smem(&S, sizeof(S));
-  sgi_poison_smem(s_dyn + lat_words, 6 * kFE * sizeof(double));
+  sgi_poison_smem(s_fused + lat_words, 6 * kFE * sizeof(double));
   __syncthreads();
   for (int k = tid; k < nlat; k += kFT) tab[k] = lat[k];
   if (tid == 0) {

@@ -2,7 +2,8 @@
     python tools/zonal_variants.py build      # here
     python tools/zonal_variants.py time       # on the GPU: C4 mesh x 1,800 latitudes
 Knobs: SGI_ZONAL_THREADS (tile = 2x edges), SGI_ZONAL_FILTER_MINB, SGI_ZONAL_FILTER_PREFETCH (0/1/2),
-SGI_ZONAL_WTHREADS (emit CTA size), SGI_ZONAL_EMIT_W2 (two queries per lane)."""
+SGI_ZONAL_WTHREADS (emit CTA size), SGI_ZONAL_EMIT_W2 (two queries per lane), SGI_ZONAL_FUSED (one
+launch), SGI_ZONAL_FT (fused kernel's CTA size; tile = 4x edges), SGI_ZONAL_STATIC, SGI_ZONAL_PARK."""
 import ctypes
 import json
 import os
@@ -14,9 +15,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "build", "zvariants")
 VARIANTS = {
-    "emit_t256": {},
-    "forward": {"SGI_ZONAL_EMIT_REVERSE": 0},
+    "fused_t256": {},
+    "fused_t512": {"SGI_ZONAL_FT": 512},
+    "three_launch": {"SGI_ZONAL_FUSED": 0},
 }
+if os.environ.get("SGI_VARIANTS"):
+    VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["SGI_VARIANTS"].split(",")}
 
 
 def build():
@@ -26,7 +30,8 @@ def build():
     for name, defs in VARIANTS.items():
         d = [f"-D{k}={v}" for k, v in defs.items()]
         lib = os.path.join(OUT, f"libsgi_{name}.so")
-        r = subprocess.run(["nvcc", *NVCC_FLAGS, *d, "-I", os.path.join(ROOT, "include"), "-o", lib,
+        flags = [f for f in NVCC_FLAGS if f not in ("-Xptxas", "-v")]
+        r = subprocess.run(["nvcc", *flags, *d, "-I", os.path.join(ROOT, "include"), "-o", lib,
                             *srcs], capture_output=True, text=True)
         assert r.returncode == 0, r.stderr
         print(name, "ok")
