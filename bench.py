@@ -99,6 +99,7 @@ class ClockSampler:
 
     def __init__(self, index: int, period: float = 0.002):
         self.samples, self.reasons, self.period = [], 0, period
+        self.power = []
         self._stop = threading.Event()
         self.max_mhz = None
         try:
@@ -115,6 +116,7 @@ class ClockSampler:
             try:
                 self.samples.append(self.nvml.nvmlDeviceGetClockInfo(self.h, self.nvml.NVML_CLOCK_SM))
                 self.reasons |= self.nvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.power.append(self.nvml.nvmlDeviceGetPowerUsage(self.h) / 1e3)
             except Exception:
                 pass
             time.sleep(self.period)
@@ -136,7 +138,9 @@ class ClockSampler:
         s = sorted(self.samples)
         med = s[len(s) // 2] if s else None
         names = [v for k, v in self.REASONS.items() if self.reasons & k and v != "gpu_idle"]
-        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(s)}
+        pw = sorted(self.power)
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(s),
+                "power_w": pw[len(pw) // 2] if pw else None}
 
     BAD = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")
 
