@@ -18,12 +18,18 @@ muts = [
  ("sqrt no h", "double t = r + h;", "double t = r;"),
  ("containment >", "int inp = (A1 >= B1) && (A2 <= B2);", "int inp = (A1 > B1) && (A2 <= B2);"),
  ("order flip", "const double* first = g1 >= 0.0 ? t.Pp : t.Pm;", "const double* first = g1 >= 0.0 ? t.Pm : t.Pp;"),
+ # double-word low part (reading R11), caught by test_oracle_dw.py's first-order bound
+ ("dw drop hi*s2", "double r = (t + dl) + (hi * s2);", "double r = (t + dl);"),
+ ("dw drop dl", "double r = (t + dl) + (hi * s2);", "double r = t + (hi * s2);"),
+ ("dw sign of s2", "double r = (t + dl) + (hi * s2);", "double r = (t + dl) - (hi * s2);"),
+ ("dw drop sigma", "double dl = (num_pair[0] - X) + num_pair[1];", "double dl = (num_pair[0] - X);"),
 ]
+TESTS = ['tests/test_oracle_accux.py', 'tests/test_oracle_eft_ops.py', 'tests/test_oracle_dw.py']
 for name, old, new in muts:
     src = open(ORIG).read()
     assert old in src, name
     open('oracle/eft_oracle.c','w').write(src.replace(old, new))
-    r = subprocess.run([sys.executable, '-m', 'pytest', 'tests/test_oracle_accux.py', 'tests/test_oracle_eft_ops.py', '-x', '-q'], capture_output=True, text=True)
+    r = subprocess.run([sys.executable, '-m', 'pytest', *TESTS, '-x', '-q'], capture_output=True, text=True)
     print(f"{name:20s} -> {'CAUGHT' if r.returncode else 'MISSED'}  {r.stdout.strip().splitlines()[-1]}")
 shutil.copy(ORIG, 'oracle/eft_oracle.c')
 os.utime('oracle/eft_oracle.c')
