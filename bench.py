@@ -108,6 +108,10 @@ class ClockSampler:
             self.nvml = pynvml
             self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            try:
+                self.limit_w = pynvml.nvmlDeviceGetEnforcedPowerLimit(self.h) / 1e3
+            except Exception:
+                self.limit_w = None
         except Exception as e:  # pragma: no cover - reported, not fatal
             self.nvml, self.err = None, str(e)
 
@@ -140,7 +144,8 @@ class ClockSampler:
         names = [v for k, v in self.REASONS.items() if self.reasons & k and v != "gpu_idle"]
         pw = sorted(self.power)
         return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(s),
-                "power_w": pw[len(pw) // 2] if pw else None}
+                "power_w": pw[len(pw) // 2] if pw else None,
+                "power_limit_w": getattr(self, "limit_w", None)}
 
     BAD = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")
 
