@@ -71,7 +71,10 @@ __device__ __forceinline__ int upper_bound(const double* t, int n, double x) {  
 // boundaries are exact binary fractions).  For x in bucket b (computed up to one bucket of
 // rounding) the answer lies between the bounds of buckets b-1 and b+2; outside [-1, 1] the
 // bracket opens to the table's ends, so any strictly increasing table is handled.
-constexpr int kBuckets = 2048;
+#ifndef SGI_ZONAL_BUCKETS
+#define SGI_ZONAL_BUCKETS 2048
+#endif
+constexpr int kBuckets = SGI_ZONAL_BUCKETS;
 
 __device__ __forceinline__ void build_buckets(int* bkt, const double* tab, int nlat) {
   for (int b = threadIdx.x; b <= kBuckets; b += blockDim.x)
@@ -163,10 +166,11 @@ __device__ __forceinline__ void candidates(const double* x, const double* tab, c
     // and search only past kStep entries (the same index either way)
     const double top = __dadd_rn(zhi, kDelta);
     constexpr int kStep = 3;
+    // the table is increasing, so the kStep tests are independent (no chain of dependent loads):
+    // k = klo + the number of the next kStep entries <= top
     int k = klo;
 #pragma unroll
-    for (int s = 0; s < kStep; ++s)
-      if (k < nlat && tab[k] <= top) ++k;
+    for (int s = 0; s < kStep; ++s) k += (klo + s < nlat && tab[klo + s] <= top) ? 1 : 0;
     if (k == klo + kStep && k < nlat && tab[k] <= top) k = bucket_search<true>(bkt, tab, nlat, top);
     kcnt = k - klo;
   }
