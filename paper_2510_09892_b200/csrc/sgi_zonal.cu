@@ -135,10 +135,13 @@ __device__ __forceinline__ double kahan_dop(double a, double b, double c, double
 // direction of n only to a few ulps: each component within 2 ulps of the exact one (kahan_dop, so
 // short arcs keep their accuracy) and heights from the device rsqrt (a few ulps, deterministic) —
 // errors ~1e-15, far below delta.
-__device__ __forceinline__ void candidates(const double* x, const double* tab, const int* bkt,
-                                           int nlat, int& klo, int& kcnt) {
-  klo = 0;
-  kcnt = 0;
+// The arc's widened z-range: lo = zlo - delta, hi = zhi + delta; mode 0 = no candidates (NaN
+// inputs), 1 = search the table, 2 = every latitude (n = 0: degenerate at every latitude).
+struct ZRange {
+  double lo, hi;
+  int mode;
+};
+__device__ __forceinline__ ZRange zrange(const double* x) {
   const double nx = kahan_dop(x[1], x[5], x[2], x[4]);
   const double ny = kahan_dop(x[2], x[3], x[0], x[5]);
   const double nz = kahan_dop(x[0], x[4], x[1], x[3]);
@@ -158,22 +161,37 @@ __device__ __forceinline__ void candidates(const double* x, const double* tab, c
     if (top_inside) zhi = fmax(zhi, h);
     else zlo = fmin(zlo, -h);
   }
-  if (nx == 0.0 && ny == 0.0 && nz == 0.0) {
-    kcnt = nlat;                                     // n = 0: degenerate at every latitude
-  } else if (finite && zhi == zhi && zlo == zlo) {   // NaN inputs: no candidates
-    klo = bucket_search<false>(bkt, tab, nlat, __dsub_rn(zlo, kDelta));
-    // first k with tab[k] > zhi + delta: mesh edges span a latitude or two, so step from klo
-    // and search only past kStep entries (the same index either way)
-    const double top = __dadd_rn(zhi, kDelta);
-    constexpr int kStep = 3;
-    // the table is increasing, so the kStep tests are independent (no chain of dependent loads):
-    // k = klo + the number of the next kStep entries <= top
-    int k = klo;
+  ZRange r;
+  r.lo = __dsub_rn(zlo, kDelta);
+  r.hi = __dadd_rn(zhi, kDelta);
+  r.mode = (nx == 0.0 && ny == 0.0 && nz == 0.0) ? 2 : (finite && zhi == zhi && zlo == zlo) ? 1 : 0;
+  return r;
+}
+
+// Candidate latitudes [klo, klo + kcnt) of a z-range: first k with tab[k] >= lo, then the first
+// with tab[k] > hi — mesh edges span a latitude or two, so the kStep entries after klo are tested
+// at once (the table is increasing: k = klo + the number of them <= hi) before a second search.
+__device__ __forceinline__ void range_search(const ZRange& r, const double* tab, const int* bkt,
+                                             int nlat, int& klo, int& kcnt) {
+  klo = 0;
+  kcnt = r.mode == 2 ? nlat : 0;
+  if (r.mode != 1) return;
+  klo = bucket_search<false>(bkt, tab, nlat, r.lo);
+  constexpr int kStep = 3;
+  int k = klo;
 #pragma unroll
-    for (int s = 0; s < kStep; ++s) k += (klo + s < nlat && tab[klo + s] <= top) ? 1 : 0;
-    if (k == klo + kStep && k < nlat && tab[k] <= top) k = bucket_search<true>(bkt, tab, nlat, top);
-    kcnt = k - klo;
-  }
+  for (int s = 0; s < kStep; ++s) k += (klo + s < nlat && tab[klo + s] <= r.hi) ? 1 : 0;
+  if (k == klo + kStep && k < nlat && tab[k] <= r.hi) k = bucket_search<true>(bkt, tab, nlat, r.hi);
+  kcnt = k - klo;
+}
+
+// Candidate latitudes [klo, klo + kcnt) of one edge (see the file comment).  The filter needs the
+// direction of n only to a few ulps: each component within 2 ulps of the exact one (kahan_dop, so
+// short arcs keep their accuracy) and heights from the device rsqrt (a few ulps, deterministic) —
+// errors ~1e-15, far below delta.
+__device__ __forceinline__ void candidates(const double* x, const double* tab, const int* bkt,
+                                           int nlat, int& klo, int& kcnt) {
+  range_search(zrange(x), tab, bkt, nlat, klo, kcnt);
 }
 
 
@@ -859,16 +877,23 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
       __syncthreads();
     }
     // ---- filter: candidate range of each edge (thread tid: edges tid, tid + kFT, ...)
+    // (the four z-ranges first — independent FP64 chains the scheduler can interleave — then the
+    // four table searches)
+    ZRange zr[kFPer];
 #pragma unroll
     for (int j = 0; j < kFPer; ++j) {
       const int l = tid + j * kFT;
-      int klo = 0, kcnt = 0;
-      if (l < nv) {
-        double x[6];
+      double x[6];
 #pragma unroll
-        for (int c = 0; c < 6; ++c) x[c] = tile[c * kFE + l];
-        candidates(x, tab, S.bkt, nlat, klo, kcnt);
-      }
+      for (int c = 0; c < 6; ++c) x[c] = tile[c * kFE + l];
+      zr[j] = zrange(x);
+      if (l >= nv) zr[j].mode = 0;
+    }
+#pragma unroll
+    for (int j = 0; j < kFPer; ++j) {
+      const int l = tid + j * kFT;
+      int klo, kcnt;
+      range_search(zr[j], tab, S.bkt, nlat, klo, kcnt);
       S.klo[l] = klo;
       S.kcnt[l] = kcnt;
     }

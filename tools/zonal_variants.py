@@ -17,8 +17,7 @@ OUT = os.path.join(ROOT, "build", "zvariants")
 VARIANTS = {
     "fused_t256": {},
     "fused_t512": {"SGI_ZONAL_FT": 512},
-    "fused_b8192": {"SGI_ZONAL_BUCKETS": 8192},
-    "fused_b4096": {"SGI_ZONAL_BUCKETS": 4096},
+
     "three_launch": {"SGI_ZONAL_FUSED": 0},
 }
 if os.environ.get("SGI_VARIANTS"):
