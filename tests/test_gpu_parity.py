@@ -197,6 +197,32 @@ def test_c5_full_size_sampled():
     assert worst <= 3.0
 
 
+def test_c5_full_size_every_query():
+    """C5 in full: all 2^30 queries of the full-size launch (the bench's launch configuration,
+    the TMA pair kernel with policy Cert) against oracle (a), bit for bit (up to the sign of zero),
+    in host chunks of 2^25 queries — the north star's "bit-identical on all five configs"."""
+    n = sgi_inputs.CONFIG_SIZES[5]
+    free, _ = torch.cuda.mem_get_info()
+    if free < n * 110:
+        pytest.skip("needs ~113 GB free HBM")
+    da, db, dz = _device_config(5, n)
+    out, cnt = sgi.intersect_arc_lat(da, db, dz, mode="eft")
+    assert sgi.dispatch_path(da, db, dz, out, cnt, mode="eft") == "tma_pair"
+    torch.cuda.synchronize()
+    chunk = 1 << 25
+    for off in range(0, n, chunk):
+        m = min(chunk, n - off)
+        a = da[:, off:off + m].contiguous().cpu().numpy()
+        b = db[:, off:off + m].contiguous().cpu().numpy()
+        z0 = dz[off:off + m].cpu().numpy()
+        got = out[:, :, off:off + m].contiguous().cpu().numpy()
+        gcnt = cnt[off:off + m].cpu().numpy()
+        ref, rcnt = oracle.intersect(oracle.MODE_EFT, a, b, z0, nthreads=NTHREADS)
+        assert np.array_equal(gcnt, rcnt), (off, int((gcnt != rcnt).sum()))
+        ok = same(got, ref)
+        assert ok.all(), (off, int((~ok).sum()))
+
+
 # ---------------------------------------------------------------------------- edge cases
 @pytest.mark.parametrize("n", [1, 31, 255, 257, 1000, 148 * 256 * 4 + 77])
 def test_ragged_sizes_and_padding(n):
