@@ -721,8 +721,9 @@ struct SmemInTwo {
 };
 
 // The edge of tile pair p: the last e with excl[e] <= p (excl[kFE] = the tile's total).
+template <int kE = kFE>
 __device__ __forceinline__ int pair_edge(const int* excl, int p) {
-  int lo = 0, hi = kFE;                      // excl[lo] <= p < excl[hi]
+  int lo = 0, hi = kE;                       // excl[lo] <= p < excl[hi]
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
     if (excl[mid] <= p) lo = mid; else hi = mid;
@@ -1051,6 +1052,262 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
   if (have_prev) flush_parked();
 }
 
+// ------------------------------------------------------- warp-specialised single-pass kernel
+// The fused kernel's work split between 8 compute warps and one control warp (288 threads,
+// 2 CTAs per SM at <= 112 registers), so the decoupled look-back leaves the compute warps'
+// critical path: the control warp draws the tickets and issues each tile's bulk copies as soon
+// as the compute warps release the tile buffer, then — once the compute warps have published the
+// tile's count — walks back over the preceding tiles' status words and hands the output base
+// over, while the compute warps run the tile's pairs.  Hand-offs are mbarriers (full: the
+// tile's bytes / its ticket; agg: the tile's count is published; prefix: the base is known;
+// free: the compute warps are done reading the tile buffer); the compute warps synchronise among
+// themselves with named barrier 1.  Results equal the fused kernel's (same filter, scan and
+// query code).
+#ifndef SGI_ZONAL_WS
+#define SGI_ZONAL_WS 1
+#endif
+#ifndef SGI_ZONAL_WS_WARPS
+#define SGI_ZONAL_WS_WARPS 7     // compute warps: 7 + 1 = 8 warps per CTA, 4 per sub-partition at
+#endif                           // 2 CTAs per SM, so 128 registers (8 + 1 would cap them at 96)
+constexpr int kWS = 32 * SGI_ZONAL_WS_WARPS; // compute threads
+constexpr int kWSThreads = kWS + 32;        // plus the control warp
+constexpr int kWSE = kFPer * kWS;           // edges per tile
+constexpr int kWSP = 2 * kWS;               // pairs per round
+
+struct WsSmem {
+  alignas(16) int kcnt[kWSE];
+  alignas(16) int excl[kWSE + 4];
+  alignas(16) int klo[kWSE];
+  int bkt[kBuckets + 1];
+  unsigned short pmap[kWSP];
+  unsigned wsum[kWS / 32];
+  long long ticket[2];
+  long long prefix;
+  int total;
+  uint64_t full, agg, pre, free_;
+};
+
+__device__ __forceinline__ void compute_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kWS) : "memory");
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kWSThreads, 2)
+sgi_zonal_ws_kernel(const double* __restrict__ va, const double* __restrict__ vb, int64_t ne,
+                    int64_t lde, const double* __restrict__ lat, int nlat, int64_t cap,
+                    int64_t* __restrict__ out_edge, int32_t* __restrict__ out_lat,
+                    uint8_t* __restrict__ out_count, double* __restrict__ out_xyz,
+                    unsigned long long* __restrict__ status, unsigned long long* d_total,
+                    bool tma) {
+  extern __shared__ __align__(128) double s_ws[];
+  __shared__ WsSmem S;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const size_t lat_words = ((size_t)nlat + 15) / 16 * 16;
+  double* tab = s_ws;
+  double* tile = s_ws + lat_words;                                // [6][kWSE]
+  sgi_poison_smem(&S, sizeof(S));
+  sgi_poison_smem(s_ws + lat_words, 6 * kWSE * sizeof(double));
+  __syncthreads();
+  for (int k = tid; k < nlat; k += kWSThreads) tab[k] = lat[k];
+  if (tid == 0) {
+    mbar_init(&S.full, 1);
+    mbar_init(&S.agg, 1);
+    mbar_init(&S.pre, 1);
+    mbar_init(&S.free_, kWS / 32);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  build_buckets(S.bkt, tab, nlat);                    // ends with a CTA barrier
+  const int64_t ntiles = (ne + kWSE - 1) / kWSE;
+  unsigned long long* ticket_ctr = status + ntiles;
+  auto plane = [&](int c) { return (c < 3 ? va : vb) + (c % 3) * lde; };
+  auto bulk_ok = [&](int64_t t) { return tma && t < ntiles && ne - t * kWSE >= kWSE; };
+  constexpr bool kW2 = MODE == sgi::MODE_EFT || MODE == sgi::MODE_EFT_LITERAL;
+
+  if (warp == kWS / 32) {
+    // ------------------------------------------------------------------ control warp
+    for (uint32_t i = 0;; ++i) {
+      const uint32_t ph = i & 1;
+      if (i > 0) mbar_wait(&S.free_, ph ^ 1);         // compute warps done with tile i - 1's buffer
+      long long t = 0;
+      if (lane == 0) {
+        t = (long long)atomicAdd(ticket_ctr, 1ull);
+        S.ticket[ph] = t;
+        if (bulk_ok(t)) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_expect_tx(&S.full, 6 * kWSE * 8);
+#pragma unroll
+          for (int c = 0; c < 6; ++c) bulk_g2s(tile + c * kWSE, plane(c) + t * kWSE, kWSE * 8, &S.full);
+        } else {
+          mbar_arrive(&S.full);                       // ticket only: the compute warps load it
+        }
+        // the tile a CTA draws next (about t + gridDim) into L2 under this one's arithmetic
+        const int64_t tn = t + gridDim.x;
+        if (bulk_ok(tn)) {
+#pragma unroll
+          for (int c = 0; c < 6; ++c)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(plane(c) + tn * kWSE),
+                         "r"(kWSE * 8) : "memory");
+        }
+      }
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t >= ntiles) break;
+      mbar_wait(&S.agg, ph);                          // the tile's count is published
+      const int T = S.total;
+      const long long pre = t == 0 ? 0 : look_back(status, t);
+      if (lane == 0) {
+        if (t > 0) st_status(status + t, kInc | (unsigned long long)(pre + T));
+        S.prefix = pre;
+        if (t == ntiles - 1) *d_total = (unsigned long long)(pre + T);
+        mbar_arrive(&S.pre);
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------------- compute warps
+  for (uint32_t i = 0;; ++i) {
+    const uint32_t ph = i & 1;
+    mbar_wait(&S.full, ph);
+    const int64_t t = S.ticket[ph];
+    if (t >= ntiles) break;
+    const int64_t e0 = t * kWSE;
+    const int nv = (int)(ne - e0 < kWSE ? ne - e0 : kWSE);
+    if (!bulk_ok(t)) {
+      for (int q = tid; q < 6 * kWSE; q += kWS) {
+        const int c = q / kWSE, l = q % kWSE;
+        tile[q] = l < nv ? plane(c)[e0 + l] : 0.0;
+      }
+      compute_sync();
+    }
+    // filter: the four z-ranges of the thread's edges, then their table searches
+    ZRange zr[kFPer];
+#pragma unroll
+    for (int j = 0; j < kFPer; ++j) {
+      const int l = tid + j * kWS;
+      double x[6];
+#pragma unroll
+      for (int c = 0; c < 6; ++c) x[c] = tile[c * kWSE + l];
+      zr[j] = zrange(x);
+      if (l >= nv) zr[j].mode = 0;
+    }
+#pragma unroll
+    for (int j = 0; j < kFPer; ++j) {
+      const int l = tid + j * kWS;
+      int klo, kcnt;
+      range_search(zr[j], tab, S.bkt, nlat, klo, kcnt);
+      S.klo[l] = klo;
+      S.kcnt[l] = kcnt;
+    }
+    compute_sync();
+    // block scan of the counts (thread tid: edges 4 tid .. 4 tid + 3) and the pair -> edge map
+    const int4 c4 = *reinterpret_cast<const int4*>(&S.kcnt[kFPer * tid]);
+    const unsigned mine = (unsigned)(c4.x + c4.y + c4.z + c4.w);
+    unsigned incl = mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += y;
+    }
+    if (lane == 31) S.wsum[warp] = incl;
+    compute_sync();
+    unsigned before = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < kWS / 32; ++w) {
+      const unsigned x = S.wsum[w];
+      before += w < warp ? x : 0;
+      total += x;
+    }
+    {
+      const int b = (int)(before + incl - mine);
+      *reinterpret_cast<int4*>(&S.excl[kFPer * tid]) =
+          make_int4(b, b + c4.x, b + c4.x + c4.y, b + c4.x + c4.y + c4.z);
+      if (tid == kWS - 1) S.excl[kWSE] = (int)total;
+      const int cs[4] = {c4.x, c4.y, c4.z, c4.w};
+      int o = b;
+#pragma unroll
+      for (int j = 0; j < kFPer; ++j) {
+        const unsigned short e = (unsigned short)(kFPer * tid + j);
+        if (cs[j] == 1) {
+          if (o < kWSP) S.pmap[o] = e;
+        } else if (cs[j] > 1) {
+          const int stop = min(o + cs[j], kWSP);
+          for (int q = o; q < stop; ++q) S.pmap[q] = e;
+        }
+        o += cs[j];
+      }
+    }
+    if (tid == 0) {
+      st_status(status + t, (t == 0 ? kInc : kAgg) | (unsigned long long)total);
+      S.total = (int)total;
+      mbar_arrive(&S.agg);
+    }
+    compute_sync();
+    const int T = (int)total;
+    // the tile's pairs, kWSP per round (thread tid: pairs r0 + tid, r0 + kWS + tid)
+    bool have_prefix = false;
+    for (int r0 = 0; r0 < T || !have_prefix; r0 += kWSP) {
+      const int p0 = r0 + tid, p1 = r0 + kWS + tid;
+      const bool v0 = p0 < T, v1 = p1 < T;
+      sgi::QueryOut o[2];
+      bool ok[2] = {true, true};
+      int le[2] = {0, 0}, kk[2] = {0, 0};
+      double zz[2] = {0.0, 0.0};
+      if (v0) {
+        SGI_CHECK(S.excl[0] == 0 && S.excl[kWSE] == T);
+        le[0] = p0 < kWSP ? (int)S.pmap[p0] : pair_edge<kWSE>(S.excl, p0);
+        kk[0] = S.klo[le[0]] + (p0 - S.excl[le[0]]);
+        le[1] = le[0];
+        kk[1] = kk[0];
+        if (v1) {
+          le[1] = p1 < kWSP ? (int)S.pmap[p1] : pair_edge<kWSE>(S.excl, p1);
+          kk[1] = S.klo[le[1]] + (p1 - S.excl[le[1]]);
+        }
+        SGI_CHECK(le[0] >= 0 && le[0] < nv && le[1] >= 0 && le[1] < nv);
+        SGI_CHECK(kk[0] >= 0 && kk[0] < nlat && kk[1] >= 0 && kk[1] < nlat);
+        zz[0] = tab[kk[0]];
+        zz[1] = tab[kk[1]];
+        if constexpr (kW2) {
+          const SmemInTwo in = {smem_u32(tile + le[0]), smem_u32(tile + le[1]), kWSE * 8};
+          sgi::QueryOut2 q;
+          const sgi::B2 okb = sgi::query_fast2<MODE>(in, sgi::W2{zz[0], zz[1]}, q);
+          o[0] = {q.p0x.x, q.p0y.x, q.p1x.x, q.p1y.x, q.count[0]};
+          o[1] = {q.p0x.y, q.p0y.y, q.p1x.y, q.p1y.y, q.count[1]};
+          ok[0] = okb.x;
+          ok[1] = okb.y;
+        } else {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (h == 1 && !v1) break;
+            const sgi::SmemIn in = {smem_u32(tile + le[h]), kWSE * 8};
+            ok[h] = sgi::query_fast<MODE>(in, zz[h], o[h]);
+          }
+        }
+      }
+      if (r0 + kWSP >= T) {                          // the last round: the tile buffer is free
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.free_);
+      }
+      if (!have_prefix) {
+        mbar_wait(&S.pre, ph);
+        have_prefix = true;
+      }
+      const long long base = S.prefix;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (!(h == 0 ? v0 : v1)) continue;
+        const int64_t j = base + (h == 0 ? p0 : p1);
+        if (j >= cap) continue;
+        if (ok[h]) store_pair(o[h], zz[h], e0 + le[h], kk[h], j, cap, out_edge, out_lat, out_count,
+                              out_xyz);
+        else emit_exact<MODE>(va, vb, lde, tab, e0 + le[h], kk[h], j, cap, out_edge, out_lat,
+                              out_count, out_xyz);
+      }
+    }
+    compute_sync();                                  // S (excl, klo, prefix) reused by the next tile
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -1107,12 +1364,14 @@ sgi_status sgi_zonal_intersect(const double* va, const double* vb, int64_t n_edg
   };
   const bool smem_tab = n_lat <= kLatSmem;
   const int64_t ntiles_f = (n_edges + kFE - 1) / kFE;
+  // status words of the single-pass kernels' tiles (+ the ticket counter)
+  const int64_t nstatus = (SGI_ZONAL_WS ? (n_edges + kWSE - 1) / kWSE : ntiles_f) + 1;
   const bool fused = SGI_ZONAL_FUSED && cap > 0 && smem_tab &&
-                     work_bytes >= (size_t)(ntiles_f + 1) * sizeof(unsigned long long);
+                     work_bytes >= (size_t)nstatus * sizeof(unsigned long long);
   if (fused) {
     // status words of the tiles and the ticket counter, zeroed for this call
     unsigned long long* status = (unsigned long long*)d_work;
-    e = cudaMemsetAsync(status, 0, (size_t)(ntiles_f + 1) * sizeof(unsigned long long), st);
+    e = cudaMemsetAsync(status, 0, (size_t)nstatus * sizeof(unsigned long long), st);
     if (e != cudaSuccess) {
       sgi_internal::set_error_msg("sgi_zonal_intersect: cudaMemsetAsync", e);
       return SGI_E_CUDA;
@@ -1145,6 +1404,29 @@ sgi_status sgi_zonal_intersect(const double* va, const double* vb, int64_t n_edg
                                       out_count, out_xyz, status, d_total, tma);
 #endif
     };
+#if SGI_ZONAL_WS
+    const size_t wsmem = ((size_t)n_lat + 15) / 16 * 16 * sizeof(double) + 6 * kWSE * sizeof(double);
+    const int64_t ntiles_w = (n_edges + kWSE - 1) / kWSE;
+    auto wk = [&](auto kernel) {
+      const size_t smem = wsmem;
+      int occ = 1;
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kWSThreads, smem);
+      const int64_t g = (int64_t)sms * (occ < 1 ? 1 : occ);
+      kernel<<<(int)(g < ntiles_w ? g : ntiles_w), kWSThreads, smem, st>>>(
+          va, vb, n_edges, ld_e, lat_z0, (int)n_lat, cap, out_edge, out_lat, out_count, out_xyz,
+          status, d_total, tma);
+    };
+    switch (mode) {
+      case SGI_MODE_NAIVE: wk(sgi_zonal_ws_kernel<sgi::MODE_NAIVE>); break;
+      case SGI_MODE_EFT: wk(sgi_zonal_ws_kernel<sgi::MODE_EFT>); break;
+      case SGI_MODE_EFT_LITERAL: wk(sgi_zonal_ws_kernel<sgi::MODE_EFT_LITERAL>); break;
+      case SGI_MODE_YAC: wk(sgi_zonal_ws_kernel<sgi::MODE_YAC>); break;
+      case SGI_MODE_BASE: wk(sgi_zonal_ws_kernel<sgi::MODE_BASE>); break;
+      default: wk(sgi_zonal_ws_kernel<sgi::MODE_NAIVE_KAHAN>); break;
+    }
+    if (false)
+#endif
     switch (mode) {
       case SGI_MODE_NAIVE: fk(sgi_zonal_fused_kernel<sgi::MODE_NAIVE>); break;
       case SGI_MODE_EFT: fk(sgi_zonal_fused_kernel<sgi::MODE_EFT>); break;
