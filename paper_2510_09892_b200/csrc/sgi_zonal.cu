@@ -1064,8 +1064,9 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
 // themselves with named barrier 1.  Results equal the fused kernel's (same filter, scan and
 // query code).
 #ifndef SGI_ZONAL_WS
-#define SGI_ZONAL_WS 1
-#endif
+#define SGI_ZONAL_WS 0   // 1: this kernel instead of the fused one (0.47 vs 0.40 ms on C4: the
+#endif                   // compute warps wait ~20% for the control warp's look-back, and 7
+                         // compute warps leave tiles of 896 edges often needing a second round)
 #ifndef SGI_ZONAL_WS_WARPS
 #define SGI_ZONAL_WS_WARPS 7     // compute warps: 7 + 1 = 8 warps per CTA, 4 per sub-partition at
 #endif                           // 2 CTAs per SM, so 128 registers (8 + 1 would cap them at 96)

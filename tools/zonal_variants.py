@@ -15,9 +15,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "build", "zvariants")
 VARIANTS = {
-    "fused_t256": {},
-    "fused_t512": {"SGI_ZONAL_FT": 512},
-
+    "ws7": {},
+    "ws8": {"SGI_ZONAL_WS_WARPS": 8},
+    "fused_t256": {"SGI_ZONAL_WS": 0},
     "three_launch": {"SGI_ZONAL_FUSED": 0},
 }
 if os.environ.get("SGI_VARIANTS"):
