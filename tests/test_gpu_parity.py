@@ -164,6 +164,7 @@ def test_c4_full_parity():
 # ------------------------------------------------- C5 (2^30) sampled, generated on the device
 def test_c5_full_size_sampled():
     n = sgi_inputs.CONFIG_SIZES[5]
+    torch.cuda.empty_cache()              # the previous 2^30 test's blocks back to the driver
     free, _ = torch.cuda.mem_get_info()
     if free < n * 110:
         pytest.skip("needs ~113 GB free HBM")
@@ -202,6 +203,7 @@ def test_c5_full_size_every_query():
     the TMA pair kernel with policy Cert) against oracle (a), bit for bit (up to the sign of zero),
     in host chunks of 2^25 queries — the north star's "bit-identical on all five configs"."""
     n = sgi_inputs.CONFIG_SIZES[5]
+    torch.cuda.empty_cache()              # the previous 2^30 test's blocks back to the driver
     free, _ = torch.cuda.mem_get_info()
     if free < n * 110:
         pytest.skip("needs ~113 GB free HBM")
