@@ -731,48 +731,52 @@ __device__ __forceinline__ int pair_edge(const int* excl, int p) {
   return lo;
 }
 
-// Exclusive output base of tile t: warp-wide look-back over the published tile counts, four
-// tiles per lane per step (128 tiles per L2 round trip).
+// Exclusive output base of tile t: warp-wide look-back over the published tile counts, kLB
+// tiles per lane per step, all loads in flight at once (32 kLB tiles per L2 round trip: the
+// nearest inclusive count is typically about one tile generation — the grid's ~300 concurrent
+// tiles — back, so one step usually ends the walk).
+#ifndef SGI_ZONAL_LB
+#define SGI_ZONAL_LB 16
+#endif
+constexpr int kLB = SGI_ZONAL_LB;
 __device__ __forceinline__ long long look_back(const unsigned long long* status, int64_t t) {
   const int lane = threadIdx.x & 31;
   long long prefix = 0;
-  for (int64_t p = t - 1;; p -= 128) {
-    unsigned long long v[4];
-    bool stop_here = false;
-    long long mine = 0;
-    // lane L covers tiles p - 4L .. p - 4L - 3 (nearest first)
+  for (int64_t p = t - 1;; p -= 32 * kLB) {
+    unsigned long long v[kLB];
+    // lane L covers tiles p - kLB L .. p - kLB L - kLB + 1 (nearest first)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t q = p - 4 * lane - j;
+    for (int j = 0; j < kLB; ++j) {
+      const int64_t q = p - kLB * lane - j;
       SGI_CHECK(q < t);
       v[j] = q >= 0 ? ld_status(status + q) : kInc;
     }
     for (;;) {
       bool missing = false;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) missing |= (v[j] >> 62) == 0;
+      for (int j = 0; j < kLB; ++j) missing |= (v[j] >> 62) == 0;
       if (!__any_sync(0xffffffffu, missing)) break;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t q = p - 4 * lane - j;
+      for (int j = 0; j < kLB; ++j) {
+        const int64_t q = p - kLB * lane - j;
         if ((v[j] >> 62) == 0) v[j] = ld_status(status + q);
       }
     }
     // the nearest inclusive entry (lowest lane, then lowest j) ends the walk
-    int jinc = 4;
+    int jinc = kLB;
 #pragma unroll
-    for (int j = 3; j >= 0; --j)
+    for (int j = kLB - 1; j >= 0; --j)
       if ((v[j] >> 62) == 2) jinc = j;
-    const unsigned inc = __ballot_sync(0xffffffffu, jinc < 4);
+    const unsigned inc = __ballot_sync(0xffffffffu, jinc < kLB);
     const int first = inc ? __ffs(inc) - 1 : 32;
+    long long mine = 0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < kLB; ++j)
       if (lane < first || (lane == first && j <= jinc)) mine += (long long)(v[j] & kValMask);
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, d);
     prefix += mine;
-    stop_here = inc != 0;
-    if (stop_here) break;
+    if (inc) break;
   }
   return prefix;
 }
