@@ -732,11 +732,11 @@ __device__ __forceinline__ int pair_edge(const int* excl, int p) {
 }
 
 // Exclusive output base of tile t: warp-wide look-back over the published tile counts, kLB
-// tiles per lane per step, all loads in flight at once (32 kLB tiles per L2 round trip: the
-// nearest inclusive count is typically about one tile generation — the grid's ~300 concurrent
-// tiles — back, so one step usually ends the walk).
+// tiles per lane per step, all loads in flight at once (32 kLB tiles per L2 round trip).  The
+// walk is bound by waiting for predecessors that have not published their counts yet, not by
+// round trips: wider windows poll more unpublished words and measured slower.
 #ifndef SGI_ZONAL_LB
-#define SGI_ZONAL_LB 16
+#define SGI_ZONAL_LB 4     // 8: 0.448 ms, 16: 0.506 ms (more polling of unpublished counts)
 #endif
 constexpr int kLB = SGI_ZONAL_LB;
 __device__ __forceinline__ long long look_back(const unsigned long long* status, int64_t t) {
