@@ -288,7 +288,7 @@ def accuracy_sample(a, b, z0, out, cnt, ref_out, ref_cnt, mode, ref_mode, idx):
     return res
 
 
-def ref_mode_chunks(L, a, b, z0, n, out, cnt, mode, ref_mode, stream, sgi, chunk=1 << 25):
+def ref_mode_chunks(a, b, z0, n, out, cnt, ref_mode, stream, sgi, chunk=1 << 25):
     """K5 statistics of the run's outputs against the other mode on the same arcs, in chunks
     (the other mode's 2^30-arc outputs would not fit beside ours): per chunk the inputs and our
     outputs copied to chunk-sized planes, the other mode into a chunk buffer, sgi_output_stats
@@ -568,8 +568,7 @@ def main():
     # K5 output statistics (outside the timed region): |P| - 1 and Pz == z0 on every stored point,
     # and the deviation from the other mode (naive-FP64 for the EFT modes) on the same arcs
     ref_mode = "naive" if mode != "naive" else "eft"
-    L = sgi._load()
-    stats, counts = ref_mode_chunks(L, a, b, z0, n, out, cnt, mode, ref_mode, stream, sgi)
+    stats, counts = ref_mode_chunks(a, b, z0, n, out, cnt, ref_mode, stream, sgi)
     if distributed:                                    # MAX of time and stats, SUM of counts (NCCL)
         sdist.reduce_after_step(t, hist, stats, counts)
     ms = float(t.item())

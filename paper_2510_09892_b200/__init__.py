@@ -229,7 +229,7 @@ def dispatch_path(a, b, z0, out_xyz, out_count, mode="eft", n=None, entry=0) -> 
                                            entry)]
 
 
-def _host_array(x, shape, dtype, name):
+def _host_array(x, shape, dtype):
     """Host buffer check for the host-buffer entry: C-contiguous numpy array or CPU tensor of
     exactly this shape and dtype (the C side reads/writes ld-pitched planes through it)."""
     import numpy as np
@@ -271,7 +271,7 @@ def intersect_arc_lat_host(a, b, z0, mode="eft", out_xyz=None, out_count=None, w
                                (z0, (ld,), np.float64, "z0"),
                                (out_xyz, (2, 3, ld), np.float64, "out_xyz"),
                                (out_count, (ld,), np.uint8, "out_count")):
-        p = _host_array(x, shape, dt, name)
+        p = _host_array(x, shape, dt)
         if p is False:
             raise ValueError(f"{name} must be a C-contiguous host {np.dtype(dt).name} array "
                              f"(numpy or CPU tensor) of shape {shape}")

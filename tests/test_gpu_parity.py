@@ -395,7 +395,6 @@ def test_bench_strong_split_dry_run():
     import bench
     from paper_2510_09892_b200 import dist as sdist
     n = (1 << 22) + 6                       # C5 layout, a ragged split
-    L = sgi._load()
     stream = torch.cuda.current_stream()
     results = {}
     for R in (1, 2, 4, 8):
@@ -413,7 +412,7 @@ def test_bench_strong_split_dry_run():
             cnt = torch.empty(m, dtype=torch.uint8, device="cuda")
             sgi.intersect_arc_lat(a, b, z0, mode="eft", out_xyz=out, out_count=cnt)
             h = sgi.count_histogram(cnt)
-            st, ct = bench.ref_mode_chunks(L, a, b, z0, m, out, cnt, "eft", "naive", stream, sgi,
+            st, ct = bench.ref_mode_chunks(a, b, z0, m, out, cnt, "naive", stream, sgi,
                                            chunk=1 << 20)
             hist += h
             stats = torch.maximum(stats, st)
