@@ -21,6 +21,8 @@ VARIANTS = {
     "stages2": {"SGI_EFT_STAGES": 2},
     "ldg_only": {"SGI_USE_TMA": 0},
     "ts_knuth": {"SGI_TS_KNUTH": 1},
+    "eft_t384": {"SGI_EFT_THREADS": 384},
+    "eft_t640": {"SGI_EFT_THREADS": 640, "SGI_EFT_STAGES": 2},
 }
 if os.environ.get("SGI_VARIANTS"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["SGI_VARIANTS"].split(",")}
