@@ -670,8 +670,8 @@ sgi_zonal_emit_warp_kernel(const double* __restrict__ va, const double* __restri
 #define SGI_ZONAL_FUSED 1
 #endif
 #ifndef SGI_ZONAL_PARK
-#define SGI_ZONAL_PARK 0     // 1: park one-round tiles' results, store after the next look-back
-#endif                       // (0.434 vs 0.421 ms: fewer barrier stalls, +9% instructions)
+#define SGI_ZONAL_PARK 1     // park one-round tiles' results, store them after the next look-back
+#endif                       // (0.389 vs 0.397 ms with the final filter; 0.434 vs 0.421 before it)
 #ifndef SGI_ZONAL_STATIC
 #define SGI_ZONAL_STATIC 0   // 1: static tiles + cooperative launch (0.478 ms vs 0.44: look-back waits)
 #endif

@@ -15,10 +15,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "build", "zvariants")
 VARIANTS = {
-    "fused_lb16": {},
-    "fused_lb4": {"SGI_ZONAL_LB": 4},
+    "fused": {},
+    "fused_park": {"SGI_ZONAL_PARK": 1},
     "fused_lb8": {"SGI_ZONAL_LB": 8},
-    "ws7_lb16": {"SGI_ZONAL_WS": 1},
+    "ws7": {"SGI_ZONAL_WS": 1},
     "three_launch": {"SGI_ZONAL_FUSED": 0},
 }
 if os.environ.get("SGI_VARIANTS"):
