@@ -23,6 +23,8 @@ VARIANTS = {
     "ts_knuth": {"SGI_TS_KNUTH": 1},
     "eft_t384": {"SGI_EFT_THREADS": 384},
     "eft_t640": {"SGI_EFT_THREADS": 640, "SGI_EFT_STAGES": 2},
+    "one_query": {"SGI_EFT_PAIR": 0},
+    "one_query_t768": {"SGI_EFT_PAIR": 0, "SGI_EFT_THREADS": 768, "SGI_EFT_STAGES": 2},
 }
 if os.environ.get("SGI_VARIANTS"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["SGI_VARIANTS"].split(",")}
