@@ -116,8 +116,11 @@ sgi_status sgi_count_histogram(const uint8_t* out_count, int64_t n,
  * d_work: caller-owned device workspace of sgi_zonal_workspace_bytes(n_edges) bytes (8 B per
  * edge for its candidate range plus 8 B per 512-edge tile, plus 8 B), 16-byte aligned
  * (SGI_E_INVALID otherwise; cudaMalloc and PyTorch allocations are).  n_lat <= 2^23.
- * Asynchronous on `stream` (three launches: filter, scan, emit).  Errors as for
- * sgi_intersect_arc_lat. */
+ * Asynchronous on `stream`: with cap > 0 and n_lat <= 4096 one single-pass launch (tiles of
+ * 1,024 edges staged by bulk copies, a decoupled look-back over per-tile counts kept in d_work,
+ * which is zeroed by a memset on `stream` first); otherwise (a count-only call, or a larger
+ * table) three launches: filter, scan, emit.  Both give the same pairs in the same order.
+ * Errors as for sgi_intersect_arc_lat. */
 sgi_status sgi_zonal_intersect(const double* va, const double* vb, int64_t n_edges,
                                int64_t ld_e, const double* lat_z0, int32_t n_lat, int64_t cap,
                                int64_t* out_edge, int32_t* out_lat, uint8_t* out_count,
