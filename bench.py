@@ -635,7 +635,7 @@ def main():
     if os.path.exists(spath):
         with open(spath) as f:
             sass = json.load(f)
-    per_q = sass.get(mode, FP64_OPS[mode])
+    per_q = sass.get(f"{mode}:{cfg}", sass.get(mode, FP64_OPS[mode]))
     hbm_bytes, ops = n * BYTES_PER_ARC, n * per_q
     t_hbm, t_alu = hbm_bytes / (peaks["hbm_gbs"] * 1e9), ops / (alu_peak * 1e12)
     traffic = None
@@ -644,7 +644,8 @@ def main():
         with open(tpath) as f:
             traffic = json.load(f).get(f"{mode}:{cfg}:{n}")
     alu = {"fp64_instr_per_query": per_q,
-           "fp64_instr_source": "ncu (profiles/fp64_sass.json)" if mode in sass else "listing",
+           "fp64_instr_source": ("ncu (profiles/fp64_sass.json)"
+                                 if mode in sass or f"{mode}:{cfg}" in sass else "listing"),
            "algorithmic_ops_per_query": FP64_OPS[mode],
            "executed_frac": ops / launch_s / 1e12 / alu_peak,
            "algorithmic_rate_tops": n * FP64_OPS[mode] / launch_s / 1e12,

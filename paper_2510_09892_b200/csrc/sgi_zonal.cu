@@ -33,6 +33,17 @@ void set_error_msg(const char* msg, cudaError_t e);   // sgi_capi.cu: sgi_last_e
 
 namespace {
 
+// the queries' policy: a two-point pair's second root goes to the fallback (sgi_eft.cuh
+// CertDefer; an edge cuts one latitude twice only near its z-extremum)
+#ifndef SGI_ZONAL_DEFER_TWO
+#define SGI_ZONAL_DEFER_TWO 1
+#endif
+#if SGI_ZONAL_DEFER_TWO
+using ZCert = sgi::CertDefer;
+#else
+using ZCert = sgi::Cert;
+#endif
+
 #ifndef SGI_ZONAL_THREADS
 #define SGI_ZONAL_THREADS 256
 #endif
@@ -473,7 +484,7 @@ __device__ __forceinline__ void run_batch(const WarpQueue& q, int n, const doubl
     // items (entry 0 otherwise; their results are never stored)
     const sgi::W2 zz = {tab[lane < n ? q.lat[lane] : 0], tab[lane + 32 < n ? q.lat[lane + 32] : 0]};
     sgi::QueryOut2 o;
-    const sgi::B2 ok = sgi::query_fast2<MODE>(in, zz, o);
+    const sgi::B2 ok = sgi::query_fast2<MODE, ZCert>(in, zz, o);
     store({o.p0x.x, o.p0y.x, o.p1x.x, o.p1y.x, o.count[0]}, zz.x, ok.x, lane);
     store({o.p0x.y, o.p0y.y, o.p1x.y, o.p1y.y, o.count[1]}, zz.y, ok.y, lane + 32);
   } else {
@@ -482,7 +493,7 @@ __device__ __forceinline__ void run_batch(const WarpQueue& q, int n, const doubl
       const sgi::SmemIn in1 = {smem_u32(&q.v[0][lane][h]), (uint32_t)sizeof(q.v[0])};
       const double z0 = tab[lane + 32 * h < n ? q.lat[lane + 32 * h] : 0];
       sgi::QueryOut o;
-      const bool ok = sgi::query_fast<MODE>(in1, z0, o);
+      const bool ok = sgi::query_fast<MODE, ZCert>(in1, z0, o);
       store(o, z0, ok, lane + 32 * h);
     }
   }
@@ -989,7 +1000,7 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
         if constexpr (kW2) {
           const SmemInTwo in = {smem_u32(tile + le[0]), smem_u32(tile + le[1]), kFE * 8};
           sgi::QueryOut2 q;
-          const sgi::B2 okb = sgi::query_fast2<MODE>(in, sgi::W2{zz[0], zz[1]}, q);
+          const sgi::B2 okb = sgi::query_fast2<MODE, ZCert>(in, sgi::W2{zz[0], zz[1]}, q);
           o[0] = {q.p0x.x, q.p0y.x, q.p1x.x, q.p1y.x, q.count[0]};
           o[1] = {q.p0x.y, q.p0y.y, q.p1x.y, q.p1y.y, q.count[1]};
           ok[0] = okb.x;
@@ -999,7 +1010,7 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
           for (int h = 0; h < 2; ++h) {
             if (h == 1 && !v1) break;
             const sgi::SmemIn in = {smem_u32(tile + le[h]), kFE * 8};
-            ok[h] = sgi::query_fast<MODE>(in, zz[h], o[h]);
+            ok[h] = sgi::query_fast<MODE, ZCert>(in, zz[h], o[h]);
           }
         }
       }
@@ -1275,7 +1286,7 @@ sgi_zonal_ws_kernel(const double* __restrict__ va, const double* __restrict__ vb
         if constexpr (kW2) {
           const SmemInTwo in = {smem_u32(tile + le[0]), smem_u32(tile + le[1]), kWSE * 8};
           sgi::QueryOut2 q;
-          const sgi::B2 okb = sgi::query_fast2<MODE>(in, sgi::W2{zz[0], zz[1]}, q);
+          const sgi::B2 okb = sgi::query_fast2<MODE, ZCert>(in, sgi::W2{zz[0], zz[1]}, q);
           o[0] = {q.p0x.x, q.p0y.x, q.p1x.x, q.p1y.x, q.count[0]};
           o[1] = {q.p0x.y, q.p0y.y, q.p1x.y, q.p1y.y, q.count[1]};
           ok[0] = okb.x;
@@ -1285,7 +1296,7 @@ sgi_zonal_ws_kernel(const double* __restrict__ va, const double* __restrict__ vb
           for (int h = 0; h < 2; ++h) {
             if (h == 1 && !v1) break;
             const sgi::SmemIn in = {smem_u32(tile + le[h]), kWSE * 8};
-            ok[h] = sgi::query_fast<MODE>(in, zz[h], o[h]);
+            ok[h] = sgi::query_fast<MODE, ZCert>(in, zz[h], o[h]);
           }
         }
       }

@@ -167,6 +167,13 @@ __global__ void devprim_kernel(int op, int k, const double* in, int width, int64
         out[2 * (i + n / 2) + 1] = ok.y ? Xm.y : sgi::qnan();
         p = ok.x ? sgi::dd{Xp.x, Xm.x} : sgi::dd{sgi::qnan(), sgi::qnan()};
       } break;
+      case 14: {   // one root at a time (policy Cert's stored-roots path): + then - root
+        bool okp = true, okm = true;
+        const double Xp = sgi::numerator_cert_one(r[0], r[1], r[2], r[3], r[4], r[5], r[6], okp, 0.0);
+        const double Xm = sgi::numerator_cert_one(r[0], r[1], r[2], r[3], r[4], sgi::flip_if(r[5], true),
+                                                  sgi::flip_if(r[6], true), okm, 0.0);
+        p = sgi::dd{okp ? Xp : sgi::qnan(), okm ? Xm : sgi::qnan()};
+      } break;
       case 13: {   // policy Cert's front: row [nx, ex, ny, ey, nz, ez, z0] -> (S2, sigma_h)
         sgi::EdgePreT<double> e;
         e.nx = {r[0], r[1]}; e.ny = {r[2], r[3]}; e.nz = {r[4], r[5]};

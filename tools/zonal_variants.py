@@ -16,6 +16,8 @@ sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "build", "zvariants")
 VARIANTS = {
     "fused": {},
+    "both_roots": {"SGI_CERT_ONE_ROOT": 0},
+    "branch_two": {"SGI_ZONAL_DEFER_TWO": 0},
     "fused_park": {"SGI_ZONAL_PARK": 1},
     "fused_lb8": {"SGI_ZONAL_LB": 8},
     "ws7": {"SGI_ZONAL_WS": 1},
