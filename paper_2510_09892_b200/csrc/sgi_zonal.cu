@@ -44,6 +44,11 @@ using ZCert = sgi::CertDefer;
 using ZCert = sgi::Cert;
 #endif
 
+// the filter takes an endpoint's z as its height when |x|^2 is within 2^-44 of 1 (zrange)
+#ifndef SGI_ZONAL_UNIT_Z
+#define SGI_ZONAL_UNIT_Z 1
+#endif
+
 #ifndef SGI_ZONAL_THREADS
 #define SGI_ZONAL_THREADS 256
 #endif
@@ -158,7 +163,21 @@ __device__ __forceinline__ ZRange zrange(const double* x) {
   const double nz = kahan_dop(x[0], x[4], x[1], x[3]);
   const double ra2 = __dadd_rn(__dadd_rn(__dmul_rn(x[0], x[0]), __dmul_rn(x[1], x[1])), __dmul_rn(x[2], x[2]));
   const double rb2 = __dadd_rn(__dadd_rn(__dmul_rn(x[3], x[3]), __dmul_rn(x[4], x[4])), __dmul_rn(x[5], x[5]));
+#if SGI_ZONAL_UNIT_Z
+  // endpoints on the unit sphere to 2^-44 (|x|^2 as computed: within 2^-44 + 4u of 1, so
+  // |z/|x| - z| <= 2^-44.9, far inside delta): z itself, no rsqrt (the usual mesh input)
+  // (the high words compared as float32 bit patterns: 0x3D300000 is 2^-44's)
+  const float lim = __int_as_float(0x3D300000);
+  const bool unit = fabsf(sgi::hi_as_float(__dadd_rn(ra2, -1.0))) < lim &&
+                    fabsf(sgi::hi_as_float(__dadd_rn(rb2, -1.0))) < lim;
+  double za = x[2], zb = x[5];
+  if (!unit) {
+    za = __dmul_rn(x[2], fast_rsqrt(ra2));
+    zb = __dmul_rn(x[5], fast_rsqrt(rb2));
+  }
+#else
   const double za = __dmul_rn(x[2], fast_rsqrt(ra2)), zb = __dmul_rn(x[5], fast_rsqrt(rb2));
+#endif
   const double g1 = __dsub_rn(__dmul_rn(nx, x[1]), __dmul_rn(ny, x[0]));
   const double g2 = __dsub_rn(__dmul_rn(nx, x[4]), __dmul_rn(ny, x[3]));
   const bool zbig = zb > za;                         // (NaN inputs are screened below)
@@ -691,7 +710,10 @@ sgi_zonal_emit_warp_kernel(const double* __restrict__ va, const double* __restri
 #endif
 constexpr int kFT = SGI_ZONAL_FT;          // threads per CTA (256: 2 CTAs per SM at <= 128 registers)
 constexpr int kFE = 4 * kFT;               // edges per tile
-constexpr int kFMinB = kFT <= 256 ? 2 : 1;
+#ifndef SGI_ZONAL_MINB
+#define SGI_ZONAL_MINB (512 / SGI_ZONAL_FT)      // 16 warps per SM at <= 128 registers
+#endif
+constexpr int kFMinB = SGI_ZONAL_MINB > 0 ? SGI_ZONAL_MINB : 1;
 constexpr int kFPer = kFE / kFT;           // edges per thread in the filter
 constexpr int kFP = 2 * kFT;               // pairs per round (two per thread)
 constexpr unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kValMask = (1ull << 62) - 1;

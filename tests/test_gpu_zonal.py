@@ -105,6 +105,25 @@ def test_degenerate_and_special_edges():
     check_against_brute(va, vb, lat, "eft", oracle.MODE_EFT)
 
 
+@pytest.mark.parametrize("kind", ["wide", "near_unit"])
+def test_non_unit_endpoints(kind):
+    """The filter's heights z/|x| for endpoints off the unit sphere: scaled by 2^[-20, 20]
+    ("wide"), or by 1 +- 2^-43 / 2^-46 / 2^-52 — either side of the filter's unit-norm shortcut
+    (|x|^2 within 2^-44 of 1: z itself) — on C1 arcs against 181 latitudes."""
+    rng = np.random.default_rng(44)
+    a, b, _ = sgi_inputs.generate_host(1, 800)
+    if kind == "wide":
+        fa, fb = (2.0 ** rng.uniform(-20, 20, (2, a.shape[1])))
+    else:
+        eps = np.array([2.0 ** -43, 2.0 ** -46, 2.0 ** -52, 0.0])
+        fa = 1 + rng.choice([-1, 1], a.shape[1]) * rng.choice(eps, a.shape[1])
+        fb = 1 + rng.choice([-1, 1], a.shape[1]) * rng.choice(eps, a.shape[1])
+    a, b = a * fa, b * fb
+    lat = np.sin(np.radians(np.linspace(-90, 90, 183)[1:-1]))
+    res, cnt = check_against_brute(a, b, lat, "eft", oracle.MODE_EFT)
+    assert (cnt != 0).sum() > 1000
+
+
 def test_repeatable_truncation_and_count_only():
     a, b, _ = sgi_inputs.generate_host(5, 20000)
     lat = sgi_inputs.latitudes(1800)
