@@ -66,10 +66,12 @@ def main():
     hi = [i for i, x in enumerate(rows) if "Address" in x and "Source" in x][0]
     h = rows[hi]
     si, ti = h.index("Source"), h.index("Thread Instructions Executed")
+    wi = h.index("Warp Stall Sampling (All Samples)")
     qsrc = os.path.join(os.path.dirname(os.path.abspath(lib)), "csrc", "sgi_query.cuh")
     fn = functions(qsrc) if os.path.exists(qsrc) else {}
     by_line, by_fn = collections.Counter(), collections.Counter()
     fp_line, fp_fn = collections.Counter(), collections.Counter()
+    st_line, st_fn = collections.Counter(), collections.Counter()
     mism = 0
     for k, x in enumerate(rows[hi + 1:]):
         if len(x) <= ti:
@@ -84,19 +86,23 @@ def main():
         isfp = x[si].split()[0].split(".")[0] in FP64 if x[si].split() else False
         by_line[key] += n
         by_fn[fkey] += n
+        st_line[key] += int(x[wi] or 0)
+        st_fn[fkey] += int(x[wi] or 0)
         if isfp:
             fp_line[key] += n
             fp_fn[fkey] += n
     if mism:
         print(f"WARNING: {mism} opcodes differ between the capture and {lib}")
     print(f"total {sum(by_line.values()):.1f} thread instr/query, FP64 {sum(fp_line.values()):.1f}")
-    print(f"{'function':28s} {'instr/q':>8s} {'fp64/q':>8s}")
+    ts = sum(st_line.values()) or 1
+    print(f"{'function':28s} {'instr/q':>8s} {'fp64/q':>8s} {'stall%':>7s}")
     for k, v in by_fn.most_common():
         if v >= 0.05:
-            print(f"{k:28s} {v:8.2f} {fp_fn[k]:8.2f}")
-    print(f"\n{'file:line':28s} {'instr/q':>8s} {'fp64/q':>8s}")
-    for k, v in by_line.most_common(top):
-        print(f"{k[0] + ':' + str(k[1]):28s} {v:8.2f} {fp_line[k]:8.2f}")
+            print(f"{k:28s} {v:8.2f} {fp_fn[k]:8.2f} {100 * st_fn[k] / ts:7.2f}")
+    print(f"\n{'file:line':28s} {'instr/q':>8s} {'fp64/q':>8s} {'stall%':>7s}")
+    keys = sorted(by_line, key=lambda k: -(by_line[k] / max(sum(by_line.values()), 1) + st_line[k] / ts))
+    for k in keys[:top]:
+        print(f"{k[0] + ':' + str(k[1]):28s} {by_line[k]:8.2f} {fp_line[k]:8.2f} {100 * st_line[k] / ts:7.2f}")
 
 
 if __name__ == "__main__":
