@@ -83,23 +83,64 @@ __device__ __forceinline__ int upper_bound(const double* t, int n, double x) {  
 
 
 // A bucket index over z in [-1, 1] turns each table search into one shared-memory lookup plus a
-// short binary search: bkt[b] = lower_bound(tab, -1 + 2b/kBuckets) for b = 0..kBuckets (the
-// boundaries are exact binary fractions).  For x in bucket b (computed up to one bucket of
-// rounding) the answer lies between the bounds of buckets b-1 and b+2; outside [-1, 1] the
-// bracket opens to the table's ends, so any strictly increasing table is handled.
+// look at the few entries of one bucket (SGI_ZONAL_EXACT_BKT, build_buckets below).  The older
+// bracket form (SGI_ZONAL_EXACT_BKT=0): bkt[b] = lower_bound(tab, -1 + 2b/kBuckets) for
+// b = 0..kBuckets (the boundaries are exact binary fractions); for x in bucket b (computed up to
+// one bucket of rounding) the answer lies between the bounds of buckets b-1 and b+2; outside
+// [-1, 1] the bracket opens to the table's ends.  Either handles any strictly increasing table.
 #ifndef SGI_ZONAL_BUCKETS
 #define SGI_ZONAL_BUCKETS 2048
 #endif
 constexpr int kBuckets = SGI_ZONAL_BUCKETS;
 
+#ifndef SGI_ZONAL_EXACT_BKT
+#define SGI_ZONAL_EXACT_BKT 1
+#endif
+
+// The bucket of x: floor((x + 1) kBuckets / 2) in float32, clamped to [0, kBuckets - 1].  Every
+// step (the conversion, the addition, the power-of-two scaling, floor, the clamp) is monotone
+// non-decreasing, so bucket(x) < bucket(y) implies x < y — which is all the exact index needs.
+__device__ __forceinline__ int bucket_of(double x) {
+  const float f = fminf(fmaxf(__fmul_rn(__fadd_rn(__double2float_rn(x), 1.0f), (float)(kBuckets / 2)),
+                              0.0f), (float)(kBuckets - 1));
+  return (int)f;
+}
+
 __device__ __forceinline__ void build_buckets(int* bkt, const double* tab, int nlat) {
+#if SGI_ZONAL_EXACT_BKT
+  // bkt[b] = the first k with bucket(tab[k]) >= b (tab increasing, so bucket(tab[k]) is too):
+  // for x with bucket(x) = b, every k < bkt[b] has tab[k] < x and every k >= bkt[b + 1] has
+  // tab[k] > x, so both searches of x only look at the entries of bucket b
+  for (int b = threadIdx.x; b <= kBuckets; b += blockDim.x) {
+    int lo = 0, hi = nlat;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (bucket_of(tab[mid]) < b) lo = mid + 1; else hi = mid;
+    }
+    bkt[b] = lo;
+  }
+#else
   for (int b = threadIdx.x; b <= kBuckets; b += blockDim.x)
     bkt[b] = lower_bound(tab, nlat, -1.0 + (double)b * (2.0 / kBuckets));
+#endif
   __syncthreads();
 }
 
 template <bool UPPER>   // false: first k with tab[k] >= x; true: first k with tab[k] > x
 __device__ __forceinline__ int bucket_search(const int* bkt, const double* tab, int nlat, double x) {
+#if SGI_ZONAL_EXACT_BKT
+  // the entries of x's bucket only (build_buckets); most buckets hold at most two latitudes,
+  // counted without a loop
+  const int b = bucket_of(x);
+  const int lo = bkt[b], n = bkt[b + 1] - lo;
+  if (n <= 2) {
+    int k = lo;
+    if (n >= 1 && (UPPER ? tab[lo] <= x : tab[lo] < x)) ++k;
+    if (n == 2 && (UPPER ? tab[lo + 1] <= x : tab[lo + 1] < x)) ++k;
+    return k;
+  }
+  return lo + (UPPER ? upper_bound(tab + lo, n, x) : lower_bound(tab + lo, n, x));
+#else
   // the bucket only has to be right to within one (the bracket spans b-1 .. b+2): float32 is
   // far more than enough (NaN never reaches here: the caller screens it)
   const float f = fminf(fmaxf(__fmul_rn(__fadd_rn((float)x, 1.0f), (float)(kBuckets / 2)), 0.0f),
@@ -108,6 +149,7 @@ __device__ __forceinline__ int bucket_search(const int* bkt, const double* tab, 
   const int lo = b >= 1 ? bkt[b - 1] : 0;
   const int hi = b + 2 <= kBuckets - 1 ? bkt[b + 2] : nlat;
   return lo + (UPPER ? upper_bound(tab + lo, hi - lo, x) : lower_bound(tab + lo, hi - lo, x));
+#endif
 }
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
@@ -207,12 +249,16 @@ __device__ __forceinline__ void range_search(const ZRange& r, const double* tab,
   kcnt = r.mode == 2 ? nlat : 0;
   if (r.mode != 1) return;
   klo = bucket_search<false>(bkt, tab, nlat, r.lo);
+#if SGI_ZONAL_EXACT_BKT
+  kcnt = bucket_search<true>(bkt, tab, nlat, r.hi) - klo;   // lo <= hi: never negative
+#else
   constexpr int kStep = 3;
   int k = klo;
 #pragma unroll
   for (int s = 0; s < kStep; ++s) k += (klo + s < nlat && tab[klo + s] <= r.hi) ? 1 : 0;
   if (k == klo + kStep && k < nlat && tab[k] <= r.hi) k = bucket_search<true>(bkt, tab, nlat, r.hi);
   kcnt = k - klo;
+#endif
 }
 
 // Candidate latitudes [klo, klo + kcnt) of one edge (see the file comment).  The filter needs the

@@ -124,6 +124,17 @@ def test_non_unit_endpoints(kind):
     assert (cnt != 0).sum() > 1000
 
 
+def test_table_with_clustered_and_out_of_range_entries():
+    """The bucket index over z in [-1, 1]: entries outside it (clamped into the end buckets),
+    many entries in one bucket (the binary-search fallback) and entries a few ulps apart."""
+    a, b, _ = sgi_inputs.generate_host(1, 600)
+    z = np.concatenate([[-3.0, -1.5, -1.0 - 2.0 ** -40], np.linspace(-1, 1, 97),
+                        0.3 + np.arange(40) * 2.0 ** -20, 0.7 + np.arange(5) * 2.0 ** -50,
+                        [1.0 + 2.0 ** -40, 2.0]])
+    lat = np.unique(z)
+    check_against_brute(a, b, lat, "eft", oracle.MODE_EFT)
+
+
 def test_repeatable_truncation_and_count_only():
     a, b, _ = sgi_inputs.generate_host(5, 20000)
     lat = sgi_inputs.latitudes(1800)

@@ -19,6 +19,7 @@ VARIANTS = {
     "both_roots": {"SGI_CERT_ONE_ROOT": 0},
     "branch_two": {"SGI_ZONAL_DEFER_TWO": 0},
     "rsqrt_z": {"SGI_ZONAL_UNIT_Z": 0},
+    "bracket_bkt": {"SGI_ZONAL_EXACT_BKT": 0},
     "ft128": {"SGI_ZONAL_FT": 128},
     "ft128_minb5": {"SGI_ZONAL_FT": 128, "SGI_ZONAL_MINB": 5},
     "ft256_minb3": {"SGI_ZONAL_MINB": 3},
