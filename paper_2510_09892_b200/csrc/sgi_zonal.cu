@@ -44,6 +44,22 @@ using ZCert = sgi::CertDefer;
 using ZCert = sgi::Cert;
 #endif
 
+// the fused kernel draws a one-round tile's next ticket before storing the parked tile (the
+// atomic in flight under that look-back and the stores) and loads the parked tile's first
+// look-back window while its next tile's bulk copies are in flight
+#ifndef SGI_ZONAL_EARLY_TK
+#define SGI_ZONAL_EARLY_TK 1
+#endif
+#ifndef SGI_ZONAL_LB
+#define SGI_ZONAL_LB 4     // 8: 0.448 ms, 16: 0.506 ms (more polling of unpublished counts)
+#endif
+#ifndef SGI_ZONAL_EARLY_TMA     // ... and issues that ticket's bulk copies once the tile is free
+#define SGI_ZONAL_EARLY_TMA 1
+#endif
+#ifndef SGI_ZONAL_LB_PREFETCH
+#define SGI_ZONAL_LB_PREFETCH 1
+#endif
+
 // the filter takes an endpoint's z as its height when |x|^2 is within 2^-44 of 1 (zrange)
 #ifndef SGI_ZONAL_UNIT_Z
 #define SGI_ZONAL_UNIT_Z 1
@@ -756,6 +772,7 @@ sgi_zonal_emit_warp_kernel(const double* __restrict__ va, const double* __restri
 #endif
 constexpr int kFT = SGI_ZONAL_FT;          // threads per CTA (256: 2 CTAs per SM at <= 128 registers)
 constexpr int kFE = 4 * kFT;               // edges per tile
+static_assert(kFT >= 64, "warp 1 draws the early ticket");
 #ifndef SGI_ZONAL_MINB
 #define SGI_ZONAL_MINB (512 / SGI_ZONAL_FT)      // 16 warps per SM at <= 128 registers
 #endif
@@ -774,6 +791,7 @@ struct FusedSmem {
   long long prefix;
   long long ticket;
   uint64_t full;
+  unsigned long long lbpre[32 * SGI_ZONAL_LB];   // warp 0's prefetched first look-back window
 };
 
 // A tile's status word carries all that is published (flag and count in one aligned 64-bit
@@ -814,11 +832,22 @@ __device__ __forceinline__ int pair_edge(const int* excl, int p) {
 // tiles per lane per step, all loads in flight at once (32 kLB tiles per L2 round trip).  The
 // walk is bound by waiting for predecessors that have not published their counts yet, not by
 // round trips: wider windows poll more unpublished words and measured slower.
-#ifndef SGI_ZONAL_LB
-#define SGI_ZONAL_LB 4     // 8: 0.448 ms, 16: 0.506 ms (more polling of unpublished counts)
-#endif
 constexpr int kLB = SGI_ZONAL_LB;
-__device__ __forceinline__ long long look_back(const unsigned long long* status, int64_t t) {
+// The first window's words as look_back loads them (lane L: tiles t-1-kLB L-j), into pre[] —
+// issued early, they are consumed (and re-polled where still missing) by look_back(..., pre).
+// A status word only moves forward (missing, aggregate, inclusive), so any value seen is usable.
+__device__ __forceinline__ void look_back_prefetch(const unsigned long long* status, int64_t t,
+                                                   unsigned long long* pre) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < kLB; ++j) {
+    const int64_t q = t - 1 - kLB * lane - j;
+    pre[lane * kLB + j] = q >= 0 ? ld_status(status + q) : kInc;
+  }
+}
+
+__device__ __forceinline__ long long look_back(const unsigned long long* status, int64_t t,
+                                               const unsigned long long* pre = nullptr) {
   const int lane = threadIdx.x & 31;
   long long prefix = 0;
   for (int64_t p = t - 1;; p -= 32 * kLB) {
@@ -828,7 +857,7 @@ __device__ __forceinline__ long long look_back(const unsigned long long* status,
     for (int j = 0; j < kLB; ++j) {
       const int64_t q = p - kLB * lane - j;
       SGI_CHECK(q < t);
-      v[j] = q >= 0 ? ld_status(status + q) : kInc;
+      v[j] = pre && p == t - 1 ? pre[lane * kLB + j] : q >= 0 ? ld_status(status + q) : kInc;
     }
     for (;;) {
       bool missing = false;
@@ -897,9 +926,21 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
   int prev_T = 0;
   bool have_prev = false;
   // look back for the parked tile, publish its inclusive count, store its results
-  auto flush_parked = [&]() {
+  bool lb_ready = false;                 // S.lbpre holds prev_t's first look-back window
+  bool pre_issued = false;               // the current tile's copies were issued by flush_parked
+  // tile tt's six bulk copies (one thread; the tile buffer must be free)
+  auto full_tile = [&](int64_t tt) { return tma && tt < ntiles && ne - tt * kFE >= kFE; };
+  auto issue_tile = [&](int64_t tt) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&S.full, 6 * kFE * 8);
+#pragma unroll
+    for (int c = 0; c < 6; ++c) bulk_g2s(tile + c * kFE, plane(c) + tt * kFE, kFE * 8, &S.full);
+  };
+  // issue_t: the next tile, whose copies thread 32 issues once every thread is past this tile's
+  // queries (the first barrier below); -1: none
+  auto flush_parked = [&](long long issue_t) {
     if (warp == 0) {
-      const long long pre = prev_t == 0 ? 0 : look_back(status, prev_t);
+      const long long pre = prev_t == 0 ? 0 : look_back(status, prev_t, lb_ready ? S.lbpre : nullptr);
       if (lane == 0) {
         if (prev_t > 0) st_status(status + prev_t, kInc | (unsigned long long)(pre + prev_T));
         S.prefix = pre;
@@ -907,6 +948,7 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
       }
     }
     __syncthreads();
+    if (tid == 32 && issue_t >= 0 && full_tile(issue_t)) issue_tile(issue_t);
     const long long base = S.prefix;
     const int64_t pe0 = prev_t * kFE;
 #pragma unroll
@@ -945,12 +987,12 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
     const int nv = (int)(ne - e0 < kFE ? ne - e0 : kFE);
     // ---- endpoints of the tile -> shared memory
     if (tma && nv == kFE) {
-      if (tid == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&S.full, 6 * kFE * 8);
-#pragma unroll
-        for (int c = 0; c < 6; ++c) bulk_g2s(tile + c * kFE, plane(c) + e0, kFE * 8, &S.full);
-      }
+      if (tid == 0 && !pre_issued) issue_tile(t);
+#if SGI_ZONAL_LB_PREFETCH
+      // the parked tile's first look-back window, loaded under the bulk copies
+      if (warp == 0 && have_prev && prev_t > 0) look_back_prefetch(status, prev_t, S.lbpre);
+      lb_ready = have_prev && prev_t > 0;
+#endif
       mbar_wait(&S.full, phase);
       phase ^= 1;
     } else {
@@ -1038,8 +1080,9 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
     // look-back is one L2 round trip instead of a wait; a larger tile flushes the parked one and
     // stores at once.
     const bool multi = !SGI_ZONAL_PARK || T > 2 * kFT;
+    pre_issued = false;
     if (multi && have_prev) {
-      flush_parked();
+      flush_parked(-1);
       have_prev = false;
     }
     bool have_prefix = !multi;
@@ -1083,8 +1126,17 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
         }
       }
       if (!multi) {
+#if !SGI_ZONAL_STATIC && SGI_ZONAL_EARLY_TK
+        long long tk = 0;               // the next ticket, in flight under the flush (warp 1)
+        if (tid == 32) tk = (long long)atomicAdd(ticket_ctr, 1ull);
+#endif
         // store the parked tile (look-back for it first), then park this one
-        if (have_prev) flush_parked();
+#if !SGI_ZONAL_STATIC && SGI_ZONAL_EARLY_TK && SGI_ZONAL_EARLY_TMA
+        if (have_prev) flush_parked(tk);
+        pre_issued = have_prev;
+#else
+        if (have_prev) flush_parked(-1);
+#endif
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int sl = h * kFT + tid;
@@ -1098,7 +1150,10 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
         prev_t = t;
         prev_T = T;
         have_prev = true;
-#if !SGI_ZONAL_STATIC
+        lb_ready = false;
+#if !SGI_ZONAL_STATIC && SGI_ZONAL_EARLY_TK
+        if (tid == 32) S.ticket = tk;
+#elif !SGI_ZONAL_STATIC
         if (tid == 0) S.ticket = (long long)atomicAdd(ticket_ctr, 1ull);
 #endif
         break;
@@ -1132,7 +1187,7 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
     }
     __syncthreads();                   // the tile buffer and S are reused by the next tile
   }
-  if (have_prev) flush_parked();
+  if (have_prev) flush_parked(-1);
 }
 
 // ------------------------------------------------------- warp-specialised single-pass kernel

@@ -20,6 +20,10 @@ VARIANTS = {
     "branch_two": {"SGI_ZONAL_DEFER_TWO": 0},
     "rsqrt_z": {"SGI_ZONAL_UNIT_Z": 0},
     "bracket_bkt": {"SGI_ZONAL_EXACT_BKT": 0},
+    "late_tk": {"SGI_ZONAL_EARLY_TK": 0},
+    "loop_top_tma": {"SGI_ZONAL_EARLY_TMA": 0},
+    "no_lb_pref": {"SGI_ZONAL_LB_PREFETCH": 0},
+    "late_tk_no_lb_pref": {"SGI_ZONAL_EARLY_TK": 0, "SGI_ZONAL_LB_PREFETCH": 0},
     "ft128": {"SGI_ZONAL_FT": 128},
     "ft128_minb5": {"SGI_ZONAL_FT": 128, "SGI_ZONAL_MINB": 5},
     "ft256_minb3": {"SGI_ZONAL_MINB": 3},
