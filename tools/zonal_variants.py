@@ -29,6 +29,9 @@ VARIANTS = {
     "ft256_minb3": {"SGI_ZONAL_MINB": 3},
     "fused_park": {"SGI_ZONAL_PARK": 1},
     "fused_lb8": {"SGI_ZONAL_LB": 8},
+    "fused_lb2": {"SGI_ZONAL_LB": 2},
+    "fused_lb4": {"SGI_ZONAL_LB": 4},
+    "fused_lb16": {"SGI_ZONAL_LB": 16},
     "ws7": {"SGI_ZONAL_WS": 1},
     "three_launch": {"SGI_ZONAL_FUSED": 0},
 }
