@@ -1085,6 +1085,12 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
     // stores at once.
     const bool multi = !SGI_ZONAL_PARK || T > 2 * kFT;
     pre_issued = false;
+#if !SGI_ZONAL_STATIC && SGI_ZONAL_EARLY_TK >= 2
+    // the next ticket, drawn before this tile's queries (warp 1): its atomic round trip is hidden
+    // under them, and the tile it names starts right after this one either way
+    long long tk = 0;
+    if (!multi && tid == 32) tk = (long long)atomicAdd(ticket_ctr, 1ull);
+#endif
     if (multi && have_prev) {
       flush_parked(-1);
       have_prev = false;
@@ -1131,8 +1137,10 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
       }
       if (!multi) {
 #if !SGI_ZONAL_STATIC && SGI_ZONAL_EARLY_TK
+#if SGI_ZONAL_EARLY_TK == 1
         long long tk = 0;               // the next ticket, in flight under the flush (warp 1)
         if (tid == 32) tk = (long long)atomicAdd(ticket_ctr, 1ull);
+#endif
 #endif
         // store the parked tile (look-back for it first), then park this one
 #if !SGI_ZONAL_STATIC && SGI_ZONAL_EARLY_TK && SGI_ZONAL_EARLY_TMA

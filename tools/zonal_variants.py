@@ -21,6 +21,7 @@ VARIANTS = {
     "rsqrt_z": {"SGI_ZONAL_UNIT_Z": 0},
     "bracket_bkt": {"SGI_ZONAL_EXACT_BKT": 0},
     "late_tk": {"SGI_ZONAL_EARLY_TK": 0},
+    "tk_before_queries": {"SGI_ZONAL_EARLY_TK": 2},
     "loop_top_tma": {"SGI_ZONAL_EARLY_TMA": 0},
     "no_lb_pref": {"SGI_ZONAL_LB_PREFETCH": 0},
     "late_tk_no_lb_pref": {"SGI_ZONAL_EARLY_TK": 0, "SGI_ZONAL_LB_PREFETCH": 0},
