@@ -25,6 +25,7 @@ VARIANTS = {
     "eft_t640": {"SGI_EFT_THREADS": 640, "SGI_EFT_STAGES": 2},
     "one_query": {"SGI_EFT_PAIR": 0},
     "both_roots": {"SGI_CERT_ONE_ROOT": 0},
+    "w2_second": {"SGI_CERT_SCALAR_SECOND": 0},
     "one_query_t768": {"SGI_EFT_PAIR": 0, "SGI_EFT_THREADS": 768, "SGI_EFT_STAGES": 2},
 }
 if os.environ.get("SGI_VARIANTS"):
