@@ -86,6 +86,21 @@ def test_c1_parity_all_modes(mode, omode):
     assert_parity(got, gcnt, ref, rcnt)
 
 
+def test_two_point_lane_mixes_on_the_pair_kernel():
+    """The pair kernel computes a query's second root only where it stores one (§5): in scalar
+    form when the other query of the thread has none, two-lane when both have two.  C3's
+    near-tangent arcs give every mix at an even, TMA-sized n (~380 both-two, ~87,000 one-two
+    lanes); all must equal oracle (a) bit for bit."""
+    n = (1 << 19) + 2
+    a, b, z0 = sgi_inputs.generate_host(3, n)
+    got, gcnt = run_gpu(a, b, z0, "eft", path="tma_pair")
+    ref, rcnt = oracle.intersect(oracle.MODE_EFT, a, b, z0, nthreads=NTHREADS)
+    assert_parity(got, gcnt, ref, rcnt)
+    c0, c1 = rcnt[0::2], rcnt[1::2]
+    assert ((c0 == 2) & (c1 == 2)).sum() > 100                       # both lanes two-lane
+    assert ((c0 == 2) & (c1 != 2)).sum() > 100 and ((c0 != 2) & (c1 == 2)).sum() > 100   # one lane
+
+
 def test_c1_eft_against_exact_oracle():
     a, b, z0 = sgi_inputs.generate_host(1, sgi_inputs.CONFIG_SIZES[1])
     got, gcnt = run_gpu(a, b, z0, "eft")
