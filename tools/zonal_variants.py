@@ -21,6 +21,7 @@ VARIANTS = {
     "rsqrt_z": {"SGI_ZONAL_UNIT_Z": 0},
     "bracket_bkt": {"SGI_ZONAL_EXACT_BKT": 0},
     "late_tk": {"SGI_ZONAL_EARLY_TK": 0},
+    "prev": None,                    # a library built by hand (e.g. the previous commit), not rebuilt
     "tk_before_queries": {"SGI_ZONAL_EARLY_TK": 2},
     "loop_top_tma": {"SGI_ZONAL_EARLY_TMA": 0},
     "no_lb_pref": {"SGI_ZONAL_LB_PREFETCH": 0},
@@ -45,6 +46,8 @@ def build():
     os.makedirs(OUT, exist_ok=True)
     srcs = [os.path.join(ROOT, "paper_2510_09892_b200", "csrc", f) for f in ("sgi_capi.cu", "sgi_zonal.cu")]
     for name, defs in VARIANTS.items():
+        if defs is None:
+            continue
         d = [f"-D{k}={v}" for k, v in defs.items()]
         lib = os.path.join(OUT, f"libsgi_{name}.so")
         flags = [f for f in NVCC_FLAGS if f not in ("-Xptxas", "-v")]
