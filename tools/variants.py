@@ -24,6 +24,7 @@ VARIANTS = {
     "eft_t384": {"SGI_EFT_THREADS": 384},
     "eft_t640": {"SGI_EFT_THREADS": 640, "SGI_EFT_STAGES": 2},
     "one_query": {"SGI_EFT_PAIR": 0},
+    "prev": None,                    # a library built by hand (e.g. the previous commit), not rebuilt
     "both_roots": {"SGI_CERT_ONE_ROOT": 0},
     "w2_second": {"SGI_CERT_SCALAR_SECOND": 0},
     "one_query_t768": {"SGI_EFT_PAIR": 0, "SGI_EFT_THREADS": 768, "SGI_EFT_STAGES": 2},
@@ -37,6 +38,8 @@ def build():
     os.makedirs(OUT, exist_ok=True)
     src = os.path.join(ROOT, "paper_2510_09892_b200", "csrc", "sgi_capi.cu")
     for name, defs in VARIANTS.items():
+        if defs is None:
+            continue
         flags = list(NVCC_FLAGS)
         if defs.get("FMAD"):                       # contraction allowed (the intrinsics must not care)
             flags = [f for f in flags if f != "-fmad=false"] + ["-fmad=true"]
