@@ -25,6 +25,7 @@ What it computes (PAPER.md, "Fast and Accurate Intersections on a Sphere"):
 from __future__ import annotations
 
 import math
+from fractions import Fraction
 from dataclasses import dataclass, field
 
 U = 2.0 ** -53
@@ -144,9 +145,12 @@ def exact_query(x1, x2, z0) -> ExactResult:
         order = [Pp if inp else Pm]
     res = ExactResult(count, ss, order, [(px / d, py / d) for px, py, d in order], (inp, inm))
     # margins of the deciding comparisons, for reporting count mismatches (floats are enough)
-    sf = math.sqrt(q.sigma / 2.0 ** (6 * L)) if q.sigma > 0 else 0.0
-    A1f, A2f = A1 / 2.0 ** (4 * L), A2 / 2.0 ** (4 * L)
-    z1f, z2f = q.X1[2] / 2.0 ** L, q.X2[2] / 2.0 ** L
+    # (integer / 2^k as a correctly rounded float: 2.0 ** k overflows for scaled inputs)
+    def f2(num, k):
+        return float(Fraction(num, 1 << k))
+    sf = math.sqrt(f2(q.sigma, 6 * L)) if q.sigma > 0 else 0.0
+    A1f, A2f = f2(A1, 4 * L), f2(A2, 4 * L)
+    z1f, z2f = f2(q.X1[2], L), f2(q.X2[2], L)
     def margin(A, B):
         den_ = abs(A) + abs(B)
         return abs(A - B) / den_ if den_ > 0 else 0.0
