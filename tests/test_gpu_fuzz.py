@@ -1,0 +1,120 @@
+"""Adversarial fuzz of the certified hot path: seeded generators aimed at the regimes where
+policy Cert's certificates (DESIGN.md §5 L7-L10) must fail or be right — near-tangent
+latitudes, near-polar and very short arcs, endpoint ties, scaled endpoints — each batch
+compared with oracle (a) element by element (counts bit-exact, points bitwise up to the sign of
+zero), on the TMA pair kernel (even n >= 2^19) and, for the EFT mode, against the exact oracle
+(b) on a sample.  Inputs stay inside the A13 contract (nonzero magnitudes in [2^-200, 2^200])."""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import exact
+
+torch = pytest.importorskip("torch")
+import paper_2510_09892_b200 as sgi  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+N = (1 << 20) + 1024          # even, TMA-sized: the production pair kernel
+NTHREADS = 16
+
+
+def unit(v):
+    return v / np.linalg.norm(v, axis=0)
+
+
+def rand_unit(rng, n):
+    return unit(rng.normal(size=(3, n)))
+
+
+def near_tangent(rng, n):
+    """z0 within a relative 10^[-16, -3] of the great circle's apex height, on both sides."""
+    a, b = rand_unit(rng, n), rand_unit(rng, n)
+    nrm = np.cross(a.T, b.T).T
+    h = np.sqrt(nrm[0] ** 2 + nrm[1] ** 2) / np.linalg.norm(nrm, axis=0)
+    eps = 10.0 ** rng.uniform(-16, -3, n) * rng.choice([-1.0, 1.0], n)
+    return a, b, np.clip(h * (1 + eps), -1, 1) * rng.choice([-1.0, 1.0], n)
+
+
+def short_arcs(rng, n):
+    """Arcs 10^[-12, -5] rad long, z0 between (or just outside) the endpoint heights."""
+    m = rand_unit(rng, n)
+    t = unit(np.cross(m.T, rng.normal(size=(n, 3))).T)
+    L = 10.0 ** rng.uniform(-12, -5, n)
+    a, b = unit(m - t * L / 2), unit(m + t * L / 2)
+    w = rng.uniform(-0.2, 1.2, n)
+    return a, b, a[2] + w * (b[2] - a[2])
+
+
+def near_polar(rng, n):
+    """Arcs passing within 10^[-12, -3] of a pole (|n_xy| small), z0 near +-1 or generic."""
+    d = 10.0 ** rng.uniform(-12, -3, n)
+    phi = rng.uniform(0, 2 * np.pi, n)
+    p = unit(np.stack([d * np.cos(phi), d * np.sin(phi), np.ones(n)]))   # near the north pole
+    q = rand_unit(rng, n)
+    s = rng.choice([-1.0, 1.0], n)
+    a, b = p * s, q
+    z0 = np.where(rng.random(n) < 0.5, s * (1 - 10.0 ** rng.uniform(-16, -2, n)),
+                  rng.uniform(-1, 1, n))
+    return a, b, z0
+
+
+def endpoint_ties(rng, n):
+    """z0 exactly an endpoint's height (the containment boundary), or one ulp off it."""
+    a, b = rand_unit(rng, n), rand_unit(rng, n)
+    z = np.where(rng.random(n) < 0.5, a[2], b[2])
+    k = rng.integers(-1, 2, n)
+    return a, b, np.where(k == 0, z, np.where(k > 0, np.nextafter(z, 2.0), np.nextafter(z, -2.0)))
+
+
+def scaled(rng, n):
+    """Endpoints scaled by 2^[-150, 150] (the arc is scale-free), z0 uniform."""
+    a, b = rand_unit(rng, n), rand_unit(rng, n)
+    a = a * 2.0 ** rng.integers(-150, 151, n)
+    b = b * 2.0 ** rng.integers(-150, 151, n)
+    return a, b, rng.uniform(-1, 1, n)
+
+
+GENS = {"near_tangent": near_tangent, "short_arcs": short_arcs, "near_polar": near_polar,
+        "endpoint_ties": endpoint_ties, "scaled": scaled}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _build():
+    sgi.build()
+
+
+def run(a, b, z0, mode):
+    da, db, dz = (torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (a, b, z0))
+    out = torch.empty((2, 3, len(z0)), dtype=torch.float64, device="cuda")
+    cnt = torch.empty(len(z0), dtype=torch.uint8, device="cuda")
+    path = sgi.dispatch_path(da, db, dz, out, cnt, mode=mode)
+    sgi.intersect_arc_lat(da, db, dz, mode=mode, out_xyz=out, out_count=cnt)
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), cnt.cpu().numpy(), path
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+@pytest.mark.parametrize("gen", sorted(GENS))
+@pytest.mark.parametrize("mode,omode", [("eft", oracle.MODE_EFT),
+                                        ("eft_literal", oracle.MODE_EFT_LITERAL)])
+def test_fuzz_against_oracle_a(gen, seed, mode, omode):
+    rng = np.random.default_rng(1000 * seed + sorted(GENS).index(gen))
+    a, b, z0 = (np.ascontiguousarray(x, dtype=np.float64) for x in GENS[gen](rng, N))
+    got, gcnt, path = run(a, b, z0, mode)
+    assert path == "tma_pair"
+    ref, rcnt = oracle.intersect(omode, a, b, z0, nthreads=NTHREADS)
+    bad = np.flatnonzero(gcnt != rcnt)
+    assert bad.size == 0, (gen, bad[:5], gcnt[bad[:5]], rcnt[bad[:5]])
+    ok = (got == ref) | (np.isnan(got) & np.isnan(ref))
+    assert ok.all(), f"{gen}: {int((~ok).sum())} coordinates differ"
+    if mode == "eft" and seed == 1:
+        # the sample of stored points within the paper's bound of the exact intersection
+        idx = rng.choice(np.flatnonzero((rcnt == 1) | (rcnt == 2)), 300, replace=False)
+        worst = 0.0
+        for i in idx:
+            ex = exact.exact_query(a[:, i], b[:, i], z0[i])
+            if ex.count != gcnt[i]:
+                continue          # endpoint ties (reading R7'): counts may differ from exact
+            for k in range(ex.count):
+                worst = max(worst, exact.err_u((got[k, 0, i], got[k, 1, i]), ex.points[k], z0[i]))
+        assert worst <= 3.0, (gen, worst)
