@@ -32,10 +32,14 @@
  * slots are the canonical quiet NaN 0x7FF8000000000000.  out_xyz z-coordinates are bit copies
  * of z0.  SGI_DEGENERATE (0xFF): n = 0 exactly (equal, antipodal or zero endpoints), or
  * n_xy = 0 with z0 = 0 (arc on the equator, which is the latitude).  n_xy = 0 with z0 != 0
- * gives count 0.  Inputs are assumed finite with nonzero component magnitudes in
- * [2^-200, 2^200], so no error term of the EFT chain underflows or overflows (the analysis
- * ignores the exponent range); NaN inputs give count 0.  No per-element condition
- * fails a call.
+ * gives count 0 (z0 compared with 0 exactly, subnormals included).  Contract: finite inputs
+ * whose endpoint components and z0 are 0 or of magnitude in [2^-120, 2^120]; then every nonzero
+ * term of the EFT chain lies in [2^-940, 2^800] (an exact cross-product component is a
+ * multiple of 2^-345; |n|^2 z0^2 >= 2^-930 is the smallest product) and every error term stays
+ * normal, so none underflows or overflows (the analysis ignores the exponent range,
+ * P:461) and the device's certified shortcuts are exact (A13).  Outside it the
+ * outputs are still computed, and NaN inputs give count 0.  No per-element condition fails a
+ * call.
  *
  * Count correctness (readings R7, R7'): containment is decided by the paper-free
  * identity P.(n x x_k) = (|n|^2/S)(z0 g_k -+ s z_k) evaluated as rounded products compared

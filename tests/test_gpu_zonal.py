@@ -135,6 +135,26 @@ def test_table_with_clustered_and_out_of_range_entries():
     check_against_brute(a, b, lat, "eft", oracle.MODE_EFT)
 
 
+def test_latitudes_at_the_filter_margins():
+    """A table built from the edges' own critical heights — endpoint z (and one ulp either side)
+    and apex heights of arcs whose extremum lies inside (and +-2 ulps) — so latitudes sit exactly
+    where the filter's z-ranges end; no nonzero pair may be missed (C1 arcs and a small mesh)."""
+    rng = np.random.default_rng(77)
+    a, b, _ = sgi_inputs.generate_host(1, 400)
+    va, vb = sgi_inputs.cubed_sphere_edges(8)
+    va, vb = np.concatenate([a, va], axis=1), np.concatenate([b, vb], axis=1)
+    n = np.cross(va.T, vb.T).T
+    apex = np.sqrt(n[0] ** 2 + n[1] ** 2) / np.linalg.norm(n, axis=0)
+    pick = rng.choice(va.shape[1], 600, replace=False)
+    z = [va[2, pick] / np.linalg.norm(va[:, pick], axis=0), vb[2, pick[:300]]]
+    z += [np.nextafter(z[0], 2.0), np.nextafter(z[0], -2.0)]
+    ap = apex[pick[:400]] * rng.choice([-1.0, 1.0], 400)
+    z += [ap, np.nextafter(np.nextafter(ap, 2.0), 2.0), np.nextafter(np.nextafter(ap, -2.0), -2.0)]
+    lat = np.unique(np.clip(np.concatenate(z), -1.0, 1.0))
+    assert 1000 < len(lat) <= 4096
+    check_against_brute(va, vb, lat, "eft", oracle.MODE_EFT)
+
+
 def test_repeatable_truncation_and_count_only():
     a, b, _ = sgi_inputs.generate_host(5, 20000)
     lat = sgi_inputs.latitudes(1800)

@@ -26,6 +26,9 @@ VARIANTS = {
     "one_query": {"SGI_EFT_PAIR": 0},
     "prev": None,                    # a library built by hand (e.g. the previous commit), not rebuilt
     "both_roots": {"SGI_CERT_ONE_ROOT": 0},
+    "same_bits": {"SGI_CERT_SAME_BITS": 1},
+    "tiny_guard": {"SGI_CERT_TINY_GUARD": 1},
+    "hiword_z0": {"SGI_EXACT_ZERO_TESTS": 0},
     "w2_second": {"SGI_CERT_SCALAR_SECOND": 0},
     "one_query_t768": {"SGI_EFT_PAIR": 0, "SGI_EFT_THREADS": 768, "SGI_EFT_STAGES": 2},
 }
