@@ -277,6 +277,9 @@ def degenerate_and_special():
         ((1, 0, 0), (0, 0, 1), float("nan")), ((float("nan"), 0, 0), (0, 0, 1), 0.5),
         ((0, 0, 1), (1, 0, 0), -0.0), ((1, 1e-300, 0), (1, -1e-300, 0), 0.0),
         ((0.3, 0.4, 0.5), (0.3, 0.4, 0.5000000000000001), 0.5),
+        # an equatorial arc (n_xy = 0) at subnormal latitudes: not the equator, count 0
+        ((0.6, 0.8, 0.0), (0.8, -0.6, 0.0), 5e-324), ((0.6, 0.8, 0.0), (0.8, -0.6, 0.0), -1e-323),
+        ((0.6, 0.8, 0.0), (0.8, -0.6, 0.0), 2.0 ** -1050),
     ]
     a = np.array([r[0] for r in rows], float).T.copy()
     b = np.array([r[1] for r in rows], float).T.copy()
