@@ -75,8 +75,35 @@ def scaled(rng, n):
     return a, b, rng.uniform(-1, 1, n)
 
 
+def specials(rng, n):
+    """Endpoints drawn from special vectors — poles, equator and axis points, their negations
+    and scaled copies, exact and one-ulp-perturbed duplicates (degenerate and antipodal arcs) —
+    against special latitudes: 0, +-1, +-subnormal (an input outside the contract the
+    containment test still handles exactly), the endpoints' own heights and one ulp off."""
+    s2 = np.sqrt(0.5)
+    base = np.array([[0, 0, 1], [0, 0, -1], [1, 0, 0], [0, 1, 0], [s2, s2, 0], [s2, 0, s2],
+                     [0.6, 0.0, 0.8], [0.0, 0.6, -0.8], [0.36, 0.48, 0.8], [1e-9, 0, 1],
+                     [0, -1e-9, -1], [0.5, 0.5, s2]], float)
+    # (one-ulp perturbations of the nonzero components only: a subnormal component is outside
+    # the A13 contract, where the high-word zero tests of n are not exact)
+    vecs = np.concatenate([base, -base, 2.0 ** 60 * base, 2.0 ** -60 * base,
+                           np.where(base != 0, np.nextafter(base, 2.0), 0.0)])
+    ia, ib = rng.integers(0, len(vecs), n), rng.integers(0, len(vecs), n)
+    dup = rng.random(n) < 0.1
+    ib = np.where(dup, ia, ib)                                # a == b: degenerate
+    a, b = vecs[ia].T.copy(), vecs[ib].T.copy()
+    anti = rng.random(n) < 0.05
+    b[:, anti] = -a[:, anti]                                  # antipodal: degenerate
+    za, zb = a[2] / np.linalg.norm(a, axis=0), b[2] / np.linalg.norm(b, axis=0)
+    zs = np.array([0.0, -0.0, 1.0, -1.0, 5e-324, -5e-324, 0.5, -0.5, 0.8, -0.8, s2])
+    k = rng.integers(0, 4, n)
+    z0 = np.where(k == 0, zs[rng.integers(0, len(zs), n)],
+                  np.where(k == 1, za, np.where(k == 2, zb, np.nextafter(za, rng.choice([-2.0, 2.0], n)))))
+    return a, b, z0
+
+
 GENS = {"near_tangent": near_tangent, "short_arcs": short_arcs, "near_polar": near_polar,
-        "endpoint_ties": endpoint_ties, "scaled": scaled}
+        "endpoint_ties": endpoint_ties, "scaled": scaled, "specials": specials}
 
 
 @pytest.fixture(scope="module", autouse=True)
