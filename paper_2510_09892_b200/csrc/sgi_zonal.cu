@@ -236,6 +236,7 @@ __device__ __forceinline__ ZRange zrange(const double* x) {
 #else
   const double za = __dmul_rn(x[2], fast_rsqrt(ra2)), zb = __dmul_rn(x[5], fast_rsqrt(rb2));
 #endif
+
   const double g1 = __dsub_rn(__dmul_rn(nx, x[1]), __dmul_rn(ny, x[0]));
   const double g2 = __dsub_rn(__dmul_rn(nx, x[4]), __dmul_rn(ny, x[3]));
   const bool zbig = zb > za;                         // (NaN inputs are screened below)
@@ -252,7 +253,15 @@ __device__ __forceinline__ ZRange zrange(const double* x) {
   ZRange r;
   r.lo = __dsub_rn(zlo, kDelta);
   r.hi = __dadd_rn(zhi, kDelta);
-  r.mode = (nx == 0.0 && ny == 0.0 && nz == 0.0) ? 2 : (finite && zhi == zhi && zlo == zlo) ? 1 : 0;
+  // every latitude when the endpoints are parallel or nearly so — (|nx| + |ny| + |nz|)^2 <=
+  // 2^-80 |a|^2 |b|^2 (n = 0: degenerate at every latitude; an arc shorter than ~1e-12 rad,
+  // or a ~ -b) — where the plain query's rounded containment may accept points anywhere on the
+  // circle (e.g. the antipode of a one-ulp arc), so the candidates stay a superset of its
+  // nonzero pairs (the comparison on the high words, ties counted as thin)
+  const double n1 = __dadd_rn(__dadd_rn(fabs(nx), fabs(ny)), fabs(nz));
+  const bool thin = sgi::hi_as_float(__dmul_rn(__dmul_rn(n1, n1), 0x1p80)) <=
+                    sgi::hi_as_float(__dmul_rn(ra2, rb2));
+  r.mode = thin ? 2 : (finite && zhi == zhi && zlo == zlo) ? 1 : 0;
   return r;
 }
 

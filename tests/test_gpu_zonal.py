@@ -155,6 +155,46 @@ def test_latitudes_at_the_filter_margins():
     check_against_brute(va, vb, lat, "eft", oracle.MODE_EFT)
 
 
+def test_special_edges_and_latitudes():
+    """Edges between special vectors (poles, axis and equator points, negated, scaled by 2^+-60,
+    one-ulp perturbed, degenerate and antipodal pairs) against a table of special latitudes and
+    the edges' own endpoint heights (+-1 ulp): conservative filter and plain-query values."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "fz", os.path.join(os.path.dirname(__file__), "test_gpu_fuzz.py"))
+    fz = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(fz)
+    rng = np.random.default_rng(5)
+    va, vb, z = fz.specials(rng, 3000)
+    zs = np.concatenate([z, np.nextafter(z, 2.0), np.nextafter(z, -2.0),
+                         [-1.0, 0.0, 1.0, 0.5, -0.5, 0.8, -0.8, np.sqrt(0.5)]])
+    lat = np.unique(np.clip(zs[np.isfinite(zs)], -1.0, 1.0))
+    lat = lat[lat != 0] if (lat == 0).sum() > 1 else lat        # (+0 and -0 compare equal)
+    assert 10 < len(lat) <= 4096
+    check_against_brute(np.ascontiguousarray(va), np.ascontiguousarray(vb), lat, "eft",
+                        oracle.MODE_EFT)
+
+
+@pytest.mark.parametrize("lo,hi", [(-16, -10), (-12, -5)])
+def test_short_and_nearly_parallel_arcs(lo, hi):
+    """Arcs 10^[lo, hi] rad long (down to a few ulps of the endpoints), some reversed into
+    nearly antipodal pairs: the plain query's rounded containment on nearly parallel endpoints
+    may report points far from the arc, and the filter must still hand it every such pair."""
+    rng = np.random.default_rng(100 + lo)
+    n = 1500
+    m = rng.normal(size=(3, n)); m /= np.linalg.norm(m, axis=0)
+    t = np.cross(m.T, rng.normal(size=(n, 3))).T; t /= np.linalg.norm(t, axis=0)
+    L = 10.0 ** rng.uniform(lo, hi, n)
+    va, vb = m - t * L / 2, m + t * L / 2
+    va /= np.linalg.norm(va, axis=0); vb /= np.linalg.norm(vb, axis=0)
+    flip = rng.random(n) < 0.2
+    vb[:, flip] = -vb[:, flip]
+    lat = np.sin(np.radians(np.linspace(-90, 90, 362)[1:-1]))
+    check_against_brute(np.ascontiguousarray(va), np.ascontiguousarray(vb), lat, "eft",
+                        oracle.MODE_EFT)
+
+
 def test_repeatable_truncation_and_count_only():
     a, b, _ = sgi_inputs.generate_host(5, 20000)
     lat = sgi_inputs.latitudes(1800)
