@@ -111,8 +111,10 @@ sgi_status sgi_count_histogram(const uint8_t* out_count, int64_t n,
  * candidate latitudes are those within delta = 2^-40 of the arc's z-range (endpoint heights
  * z/|x| and, when the great circle's extremum lies inside the arc, the apex height
  * sqrt(|n_xy|^2/|n|^2), from a normal accurate to 2 ulps per component); an edge with n = 0
- * (degenerate at every latitude) has every latitude as a candidate.  Every (edge, latitude) whose query has a
- * nonzero count is a candidate; candidates within delta of the range may have count 0.
+ * (degenerate at every latitude) or nearly parallel endpoints ((|nx|+|ny|+|nz|)^2 <=
+ * 2^-80 |a|^2 |b|^2, where the query's rounded containment may accept points far from the arc)
+ * has every latitude as a candidate.  Every (edge, latitude) whose query has a nonzero count is
+ * a candidate; candidates within delta of the range (and those of such edges) may have count 0.
  * Candidate pair j (edge-major, latitude ascending; deterministic) is written to out_edge[j],
  * out_lat[j], out_count[j] and out_xyz[(slot*3 + c)*cap + j], bit-identical to
  * sgi_intersect_arc_lat on (va_e, vb_e, lat_z0[k]) in `mode`.  Pairs j >= cap are not written;
