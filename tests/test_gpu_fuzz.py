@@ -121,15 +121,20 @@ def run(a, b, z0, mode):
     return out.cpu().numpy(), cnt.cpu().numpy(), path
 
 
-@pytest.mark.parametrize("seed", [1, 2, 3])
+# the EFT modes on three seeds, the formula variants on one
+CASES = ([(m, o, sd) for m, o in (("eft", oracle.MODE_EFT), ("eft_literal", oracle.MODE_EFT_LITERAL))
+          for sd in (1, 2, 3)] +
+         [(m, o, 1) for m, o in (("naive", oracle.MODE_NAIVE), ("yac", oracle.MODE_YAC),
+                                 ("base", oracle.MODE_BASE), ("naive_kahan", oracle.MODE_NAIVE_KAHAN))])
+
+
 @pytest.mark.parametrize("gen", sorted(GENS))
-@pytest.mark.parametrize("mode,omode", [("eft", oracle.MODE_EFT),
-                                        ("eft_literal", oracle.MODE_EFT_LITERAL)])
+@pytest.mark.parametrize("mode,omode,seed", CASES)
 def test_fuzz_against_oracle_a(gen, seed, mode, omode):
     rng = np.random.default_rng(1000 * seed + sorted(GENS).index(gen))
     a, b, z0 = (np.ascontiguousarray(x, dtype=np.float64) for x in GENS[gen](rng, N))
     got, gcnt, path = run(a, b, z0, mode)
-    assert path == "tma_pair"
+    assert path == ("tma_pair" if mode in ("eft", "eft_literal") else "tma")
     ref, rcnt = oracle.intersect(omode, a, b, z0, nthreads=NTHREADS)
     bad = np.flatnonzero(gcnt != rcnt)
     assert bad.size == 0, (gen, bad[:5], gcnt[bad[:5]], rcnt[bad[:5]])
