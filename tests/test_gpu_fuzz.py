@@ -151,3 +151,26 @@ def test_fuzz_against_oracle_a(gen, seed, mode, omode):
             for k in range(ex.count):
                 worst = max(worst, exact.err_u((got[k, 0, i], got[k, 1, i]), ex.points[k], z0[i]))
         assert worst <= 3.0, (gen, worst)
+
+
+@pytest.mark.parametrize("gen", sorted(GENS))
+@pytest.mark.parametrize("mode,omode", [("eft", oracle.MODE_EFT),
+                                        ("eft_literal", oracle.MODE_EFT_LITERAL)])
+def test_fuzz_double_word_and_host_entry(gen, mode, omode):
+    """The same adversarial batches through the double-word entry (hi and lo parts bit-equal
+    to oracle (a)'s) and through the host-buffer entry (bit-equal to the device entry)."""
+    rng = np.random.default_rng(7000 + sorted(GENS).index(gen))
+    a, b, z0 = (np.ascontiguousarray(x, dtype=np.float64) for x in GENS[gen](rng, N))
+    da, db, dz = (torch.from_numpy(x).cuda() for x in (a, b, z0))
+    out, lo, cnt = sgi.intersect_arc_lat_dw(da, db, dz, mode=mode)
+    torch.cuda.synchronize()
+    ref, rlo, rcnt = oracle.intersect_dw(omode, a, b, z0, nthreads=NTHREADS)
+    assert np.array_equal(cnt.cpu().numpy(), rcnt)
+    for got, want in ((out.cpu().numpy(), ref), (lo.cpu().numpy(), rlo)):
+        assert ((got == want) | (np.isnan(got) & np.isnan(want))).all()
+    dev, dcnt, _ = run(a, b, z0, mode)
+    hout = np.empty((2, 3, N))
+    hcnt = np.empty(N, dtype=np.uint8)
+    sgi.intersect_arc_lat_host(a, b, z0, mode=mode, out_xyz=hout, out_count=hcnt)
+    assert np.array_equal(hcnt, dcnt)
+    assert ((hout == dev) | (np.isnan(hout) & np.isnan(dev))).all()
