@@ -32,6 +32,8 @@ VARIANTS = {
     "fused_park": {"SGI_ZONAL_PARK": 1},
     "fused_lb8": {"SGI_ZONAL_LB": 8},
     "fused_lb2": {"SGI_ZONAL_LB": 2},
+    "b4096": {"SGI_ZONAL_BUCKETS": 4096},
+    "b1024": {"SGI_ZONAL_BUCKETS": 1024},
     "fused_lb4": {"SGI_ZONAL_LB": 4},
     "fused_lb16": {"SGI_ZONAL_LB": 16},
     "ws7": {"SGI_ZONAL_WS": 1},
