@@ -1247,7 +1247,7 @@ struct WsSmem {
   uint64_t full, agg, pre, free_;
 };
 
-__device__ __forceinline__ void compute_sync() {
+[[maybe_unused]] __device__ __forceinline__ void compute_sync() {   // (SGI_ZONAL_WS only)
   asm volatile("bar.sync 1, %0;" ::"n"(kWS) : "memory");
 }
 
