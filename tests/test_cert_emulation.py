@@ -57,6 +57,20 @@ def numerators_cert(F, eF, v, ev, z0, s, es):
     return out, sums, abs(P1) + abs(P3)
 
 
+def numerator_cert_one(F, eF, v, ev, z0, s, es):
+    """Emulation of sgi_query.cuh numerator_cert_one (es_dev = 0): one root, its sign folded
+    into s and es."""
+    P1, e1 = tp(F, z0)
+    P3, e3 = tp(v, s)
+    c = fma(eF, z0, e1)
+    w = fma(ev, es, fma(v, es, fma(ev, s, e3)))
+    M2 = (abs(P1) + abs(P3)) * 2.0 ** -97
+    H, q = ts(P1, P3)
+    sig = (q + c) + w
+    up, dn = H + (sig + M2), H + (sig - M2)
+    return up if up - dn == 0 else None
+
+
 def cert_front(nx, ex, ny, ey, nz, ez, z0):
     """Emulation of cert_sums + cert_sigma: (S2 or None, sigma_h or None) and the sums."""
     a2, b2, c2 = tp(nx, nx), tp(ny, ny), tp(nz, nz)
@@ -131,6 +145,27 @@ def test_numerator_certificate(near_ties):
         assert fired > 300
     else:
         assert fired == 0
+
+
+@pytest.mark.parametrize("near_ties", [False, True])
+def test_one_root_numerator_is_the_two_root_one(near_ties):
+    """L10: the - root's certified numerator computed as the + root's with s and e_s negated
+    (TwoProd(v, -s) = -TwoProd(v, s), RN odd) equals the two-root form bit for bit, certificate
+    decision included — also on rows placed on rounding boundaries."""
+    rng = np.random.default_rng(41 + near_ties)
+    rows = numerator_rows(rng, 3000, near_ties)
+    fired = 0
+    for r in rows:
+        both, _, _ = numerators_cert(*r)
+        F, eF, v, ev, z0, s, es = r
+        one = (numerator_cert_one(F, eF, v, ev, z0, s, es),
+               numerator_cert_one(F, eF, v, ev, z0, -s, -es))
+        for k in range(2):
+            assert (one[k] is None) == (both[k] is None)
+            if one[k] is not None:
+                assert math.copysign(1.0, one[k]) == math.copysign(1.0, both[k]) and one[k] == both[k]
+            fired += one[k] is None
+    assert (fired > 300) if near_ties else fired == 0
 
 
 def front_rows(rng, n, target):
