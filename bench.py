@@ -649,6 +649,10 @@ def main():
            "algorithmic_ops_per_query": FP64_OPS[mode],
            "executed_frac": ops / launch_s / 1e12 / alu_peak,
            "algorithmic_rate_tops": n * FP64_OPS[mode] / launch_s / 1e12,
+           "algorithmic_note": ("the listing's operations per second; it can exceed the "
+                                "instruction peak because the shipped kernel executes fewer "
+                                "FP64 instructions than the listing has operations (policy "
+                                "Cert, DESIGN.md §5) — executed_frac is the pipe's share"),
            "peak": alu_peak, "unit": "T FP64 instr/s",
            "peak_source": f"{sms} SM x 64 FP64 lanes x {peaks['sm_max_mhz']:.0f} MHz "
                           "(tools/fp64_peak.cu measures 18.56 T DADD/s: profiles/r02/)"}
