@@ -8,6 +8,9 @@ TAG=${1:-r02}
 OUT=gpurun_out
 mkdir -p $OUT
 { free -g; nproc; nvidia-smi --query-gpu=name,clocks.max.sm,memory.total --format=csv; } > $OUT/${TAG}_host.txt 2>&1
+# the FP64 microbenchmarks (git-ignored binaries): build them if absent
+[ -x tools/fp64_peak ] || nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/fp64_peak tools/fp64_peak.cu
+[ -x tools/fp64_mix ] || nvcc -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false -o tools/fp64_mix tools/fp64_mix.cu
 ./tools/fp64_peak > $OUT/${TAG}_fp64_peak.json 2>&1
 ./tools/fp64_mix > $OUT/${TAG}_fp64_mix.txt 2>&1
 ARGS="--steps 5 --warmup 3 --e2e-steps 0 --no-cpu-baseline --no-accuracy"
