@@ -521,6 +521,9 @@ def main():
     ws, rank, local = sdist.env()
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    if local >= torch.cuda.device_count():
+        raise SystemExit(f"bench.py: rank {rank} has LOCAL_RANK {local} but only "
+                         f"{torch.cuda.device_count()} GPU(s) are visible (one rank per GPU)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     distributed = "RANK" in os.environ                  # launched by torchrun (any world size)
