@@ -27,6 +27,19 @@
 #include "sgi_query.cuh"
 #include "sgi_tma.cuh"
 
+#if SGI_ZONAL_COUNT_FALLBACKS     // measurement only (tools/zonal_variants.py): emit_exact calls
+__device__ unsigned long long g_zonal_fallbacks = 0;
+extern "C" unsigned long long sgi_debug_zonal_fallbacks(int reset) {
+  unsigned long long v = 0;
+  cudaMemcpyFromSymbol(&v, g_zonal_fallbacks, sizeof(v));
+  if (reset) {
+    const unsigned long long z = 0;
+    cudaMemcpyToSymbol(g_zonal_fallbacks, &z, sizeof(z));
+  }
+  return v;
+}
+#endif
+
 namespace sgi_internal {
 void set_error_msg(const char* msg, cudaError_t e);   // sgi_capi.cu: sgi_last_error() text
 }
@@ -52,6 +65,11 @@ using ZCert = sgi::Cert;
 #endif
 #ifndef SGI_ZONAL_LB
 #define SGI_ZONAL_LB 1     // tiles per lane per look-back step (4: 0.3485 ms, 2: 0.3446, 1: 0.3412)
+#endif
+// a pair whose certificates fail: Fast policy first (1; measured 0.363 vs 0.345 ms — C4's 0.12%
+// fallback pairs are the ones whose Fast guards fail too) or the Exact policy at once (0)
+#ifndef SGI_ZONAL_FALLBACK_FAST
+#define SGI_ZONAL_FALLBACK_FAST 0
 #endif
 #ifndef SGI_ZONAL_EARLY_TMA     // ... and issues that ticket's bulk copies once the tile is free
 #define SGI_ZONAL_EARLY_TMA 1
@@ -542,8 +560,17 @@ __device__ __noinline__ void emit_exact(const double* __restrict__ va,
                                         double* __restrict__ out_xyz) {
   const sgi::RegIn r = {{va[e], va[lde + e], va[2 * lde + e], vb[e], vb[lde + e], vb[2 * lde + e]}};
   const double z0 = tab[k];
+#if SGI_ZONAL_COUNT_FALLBACKS
+  atomicAdd(&::g_zonal_fallbacks, 1ull);
+#endif
   sgi::QueryOut o;
+#if SGI_ZONAL_FALLBACK_FAST
+  // the listing's sequence with the branch-free division/sqrt (policy Fast), the IEEE
+  // intrinsics only if one of its guards fails — as the batch kernel's fallback queue
+  if (!sgi::query_with<MODE, sgi::Fast>(r, z0, o)) sgi::query_exact<MODE>(r, z0, o);
+#else
   sgi::query_exact<MODE>(r, z0, o);
+#endif
   store_pair(o, z0, e, k, j, cap, out_edge, out_lat, out_count, out_xyz);
 }
 

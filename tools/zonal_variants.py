@@ -16,6 +16,8 @@ sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "build", "zvariants")
 VARIANTS = {
     "fused": {},
+    "count_fallbacks": {"SGI_ZONAL_COUNT_FALLBACKS": 1},
+    "fallback_fast": {"SGI_ZONAL_FALLBACK_FAST": 1},
     "both_roots": {"SGI_CERT_ONE_ROOT": 0},
     "branch_two": {"SGI_ZONAL_DEFER_TWO": 0},
     "rsqrt_z": {"SGI_ZONAL_UNIT_Z": 0},
