@@ -40,6 +40,16 @@ extern "C" unsigned long long sgi_debug_zonal_fallbacks(int reset) {
 }
 #endif
 
+#if SGI_CERT_DEBUG_REASONS
+extern "C" void sgi_debug_cert_reasons(unsigned long long* out5, int reset) {
+  cudaMemcpyFromSymbol(out5, ::g_cert_reasons, 5 * sizeof(unsigned long long));
+  if (reset) {
+    const unsigned long long z[5] = {0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(::g_cert_reasons, z, sizeof(z));
+  }
+}
+#endif
+
 namespace sgi_internal {
 void set_error_msg(const char* msg, cudaError_t e);   // sgi_capi.cu: sgi_last_error() text
 }

@@ -27,6 +27,7 @@ VARIANTS = {
     "prev": None,                    # a library built by hand (e.g. the previous commit), not rebuilt
     "both_roots": {"SGI_CERT_ONE_ROOT": 0},
     "same_bits": {"SGI_CERT_SAME_BITS": 1},
+    "zero_div_all": {"SGI_CERT_ZERO_DIV_ALL": 1},
     "tiny_guard": {"SGI_CERT_TINY_GUARD": 1},
     "hiword_z0": {"SGI_EXACT_ZERO_TESTS": 0},
     "w2_second": {"SGI_CERT_SCALAR_SECOND": 0},
