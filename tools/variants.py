@@ -28,6 +28,7 @@ VARIANTS = {
     "both_roots": {"SGI_CERT_ONE_ROOT": 0},
     "same_bits": {"SGI_CERT_SAME_BITS": 1},
     "zero_div_all": {"SGI_CERT_ZERO_DIV_ALL": 1},
+    "count_reasons": {"SGI_CERT_DEBUG_REASONS": 1, "SGI_DBG_CLOCK": 1},
     "tiny_guard": {"SGI_CERT_TINY_GUARD": 1},
     "hiword_z0": {"SGI_EXACT_ZERO_TESTS": 0},
     "w2_second": {"SGI_CERT_SCALAR_SECOND": 0},
