@@ -78,6 +78,9 @@ using ZCert = sgi::Cert;
 #endif
 // a pair whose certificates fail: Fast policy first (1; measured 0.363 vs 0.345 ms — C4's 0.12%
 // fallback pairs are the ones whose Fast guards fail too) or the Exact policy at once (0)
+#ifndef SGI_ZONAL_ONE_BARRIER    // one barrier between tiles instead of two back to back
+#define SGI_ZONAL_ONE_BARRIER 1
+#endif
 #ifndef SGI_ZONAL_FALLBACK_FAST
 #define SGI_ZONAL_FALLBACK_FAST 0
 #endif
@@ -1243,7 +1246,10 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
                               out_count, out_xyz);
       }
     }
+#if SGI_ZONAL_STATIC || !SGI_ZONAL_ONE_BARRIER
     __syncthreads();                   // the tile buffer and S are reused by the next tile
+#endif
+    // (otherwise the loop top's barrier, right after, is the one that guards that reuse)
   }
   if (have_prev) flush_parked(-1);
 }
