@@ -78,6 +78,12 @@ using ZCert = sgi::Cert;
 #endif
 // a pair whose certificates fail: Fast policy first (1; measured 0.363 vs 0.345 ms — C4's 0.12%
 // fallback pairs are the ones whose Fast guards fail too) or the Exact policy at once (0)
+// the filter's edges per thread consecutive, counts kept in registers and one barrier fewer (1;
+// measured 0.348 vs 0.339 ms: 2-way bank conflicts on the 128-bit reads and longer live ranges)
+// or strided (0)
+#ifndef SGI_ZONAL_CONSEC_FILTER
+#define SGI_ZONAL_CONSEC_FILTER 0
+#endif
 #ifndef SGI_ZONAL_ONE_BARRIER    // one barrier between tiles instead of two back to back
 #define SGI_ZONAL_ONE_BARRIER 1
 #endif
@@ -1055,6 +1061,36 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
       }
       __syncthreads();
     }
+#if SGI_ZONAL_CONSEC_FILTER
+    // ---- filter: candidate range of each edge (thread tid: edges 4 tid .. 4 tid + 3, read as
+    // 128-bit pairs; the counts stay in registers for the scan, so no barrier between them)
+    // (the four z-ranges first — independent FP64 chains the scheduler can interleave — then the
+    // four table searches)
+    static_assert(kFPer == 4, "four consecutive edges per thread");
+    ZRange zr[kFPer];
+    {
+      double xs[6][kFPer];
+#pragma unroll
+      for (int c = 0; c < 6; ++c) {
+        const double2 u = *reinterpret_cast<const double2*>(&tile[c * kFE + kFPer * tid]);
+        const double2 v = *reinterpret_cast<const double2*>(&tile[c * kFE + kFPer * tid + 2]);
+        xs[c][0] = u.x; xs[c][1] = u.y; xs[c][2] = v.x; xs[c][3] = v.y;
+      }
+#pragma unroll
+      for (int j = 0; j < kFPer; ++j) {
+        double x[6];
+#pragma unroll
+        for (int c = 0; c < 6; ++c) x[c] = xs[c][j];
+        zr[j] = zrange(x);
+        if (kFPer * tid + j >= nv) zr[j].mode = 0;
+      }
+    }
+    int klo4[kFPer], c4a[kFPer];
+#pragma unroll
+    for (int j = 0; j < kFPer; ++j) range_search(zr[j], tab, S.bkt, nlat, klo4[j], c4a[j]);
+    *reinterpret_cast<int4*>(&S.klo[kFPer * tid]) = make_int4(klo4[0], klo4[1], klo4[2], klo4[3]);
+    const int4 c4 = make_int4(c4a[0], c4a[1], c4a[2], c4a[3]);
+#else
     // ---- filter: candidate range of each edge (thread tid: edges tid, tid + kFT, ...)
     // (the four z-ranges first — independent FP64 chains the scheduler can interleave — then the
     // four table searches)
@@ -1077,6 +1113,7 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
       S.kcnt[l] = kcnt;
     }
     __syncthreads();
+#endif
     // tile t + gridDim.x (about the ticket some CTA draws next) into L2 under this tile's
     // arithmetic, so that CTA's bulk copies hit L2
     if (tid == 0 && tma && t + gridDim.x < ntiles && ne - (t + gridDim.x) * kFE >= kFE) {
@@ -1086,7 +1123,9 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
                      "r"(kFE * 8) : "memory");
     }
     // ---- block scan of the counts (thread tid: edges 4 tid .. 4 tid + 3)
+#if !SGI_ZONAL_CONSEC_FILTER
     const int4 c4 = *reinterpret_cast<const int4*>(&S.kcnt[kFPer * tid]);
+#endif
     const unsigned mine = (unsigned)(c4.x + c4.y + c4.z + c4.w);
     unsigned incl = mine;
 #pragma unroll
