@@ -28,6 +28,9 @@ VARIANTS = {
     "both_roots": {"SGI_CERT_ONE_ROOT": 0},
     "same_bits": {"SGI_CERT_SAME_BITS": 1},
     "zero_div_all": {"SGI_CERT_ZERO_DIV_ALL": 1},
+    "small_s2_50": {"SGI_CERT_SMALL_S2": "0x1p50"},
+    "small_s2_70": {"SGI_CERT_SMALL_S2": "0x1p70"},
+    "small_s2_80": {"SGI_CERT_SMALL_S2": "0x1p80"},
     "count_reasons": {"SGI_CERT_DEBUG_REASONS": 1, "SGI_DBG_CLOCK": 1},
     "tiny_guard": {"SGI_CERT_TINY_GUARD": 1},
     "hiword_z0": {"SGI_EXACT_ZERO_TESTS": 0},
