@@ -84,6 +84,9 @@ using ZCert = sgi::Cert;
 #ifndef SGI_ZONAL_CONSEC_FILTER
 #define SGI_ZONAL_CONSEC_FILTER 0
 #endif
+#ifndef SGI_ZONAL_L2_PREFETCH    // tile t + gridDim prefetched into L2 under tile t's arithmetic
+#define SGI_ZONAL_L2_PREFETCH 1
+#endif
 #ifndef SGI_ZONAL_ONE_BARRIER    // one barrier between tiles instead of two back to back
 #define SGI_ZONAL_ONE_BARRIER 1
 #endif
@@ -1116,7 +1119,8 @@ sgi_zonal_fused_kernel(const double* __restrict__ va, const double* __restrict__
 #endif
     // tile t + gridDim.x (about the ticket some CTA draws next) into L2 under this tile's
     // arithmetic, so that CTA's bulk copies hit L2
-    if (tid == 0 && tma && t + gridDim.x < ntiles && ne - (t + gridDim.x) * kFE >= kFE) {
+    if (SGI_ZONAL_L2_PREFETCH && tid == 0 && tma && t + gridDim.x < ntiles &&
+        ne - (t + gridDim.x) * kFE >= kFE) {
 #pragma unroll
       for (int c = 0; c < 6; ++c)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(plane(c) + (t + gridDim.x) * kFE),

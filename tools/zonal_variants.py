@@ -20,6 +20,7 @@ VARIANTS = {
     "count_reasons": {"SGI_ZONAL_COUNT_FALLBACKS": 1, "SGI_CERT_DEBUG_REASONS": 1},
     "zero_div_off": {"SGI_CERT_ZERO_DIV": 0},
     "two_barriers": {"SGI_ZONAL_ONE_BARRIER": 0},
+    "no_l2_prefetch": {"SGI_ZONAL_L2_PREFETCH": 0},
     "consec_filter": {"SGI_ZONAL_CONSEC_FILTER": 1},
     "fallback_fast": {"SGI_ZONAL_FALLBACK_FAST": 1},
     "both_roots": {"SGI_CERT_ONE_ROOT": 0},
